@@ -1,0 +1,170 @@
+/*
+ * tilemul_b200 — C ABI of the B200-native MOMMS GEMM (C += A·B, FP64,
+ * column-major), a drop-in for the reference toolkit's execution path.
+ *
+ * Every entry point replaces one reference interface, cited as
+ * /root/reference/proj/<file>:<line>. Plain pointers and sizes only; device
+ * pointers are CUDA global-memory addresses, `stream` is a cudaStream_t
+ * (NULL = legacy default stream).
+ *
+ * Status codes (the reference CLI's exit codes, tools/tilemul_main.cpp:519-535,
+ * extended): 0 ok; 1 a family/blocksize rule is broken (ParseError,
+ * ValidationFailure, InfeasibleError — tm_last_rules() lists the rule ids);
+ * 2 usage/config error (std::invalid_argument, ConfigError); 3 CUDA runtime
+ * error. The error text of the calling thread is in tm_last_error().
+ */
+#ifndef TILEMUL_B200_H
+#define TILEMUL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One memory level; replaces tilemul::CacheLevel (include/tilemul/cache.hpp:12-19).
+ * Capacity in elements of the operand type (FP64 = 8 bytes). */
+typedef struct {
+    int64_t capacity_elements;
+    int64_t granularity;
+    int32_t inclusive;
+    int32_t write_allocate;
+    int32_t write_back;
+} tm_level;
+
+/* One blocksize entry; replaces BlocksizeSet::set(level, dim, value)
+ * (include/tilemul/blocksizes.hpp:30-33). dim is 'm', 'n' or 'k'. */
+typedef struct {
+    int32_t level;
+    char dim;
+    int64_t value;
+} tm_blocksize;
+
+/* One partition loop of the nest, outermost first; replaces NestStep
+ * (include/tilemul/blocksizes.hpp:428-434). */
+typedef struct {
+    int32_t level;
+    char dim;
+    int64_t blocksize;
+    int32_t cap;
+} tm_loop;
+
+/* One planned level of a family member; replaces LevelPlan
+ * (include/tilemul/descriptor.hpp:18-25). */
+typedef struct {
+    int32_t level;
+    char resident; /* 'A' 'B' 'C' */
+    char outer_dim;
+    char inner_dim;
+} tm_tier;
+
+/* Derivation knobs; replaces AccessCosts + DeriveOptions + MicroTile
+ * (include/tilemul/blocksizes.hpp:59-87). */
+typedef struct {
+    double slack;   /* default 1/16 */
+    int64_t m_r;    /* register tile (the CTA's C tile on the GPU) */
+    int64_t n_r;
+    double beta_a, beta_b, beta_c;
+} tm_derive_opts;
+
+/* Kernel numerics. All accumulate every C entry in ascending k from C's
+ * incoming value (the reference's cell semantics, exec.hpp:35-46). */
+enum {
+    TM_NUMERICS_DMMA = 0,  /* FP64 tensor pipe, mma.sync m8n8k4 (SASS DMMA.8x8x4) */
+    TM_NUMERICS_FMA = 1,   /* DFMA chain, one rounding per step: bit-exact vs a sequential fma oracle */
+    TM_NUMERICS_EXACT = 2  /* DMUL then DADD, two roundings: bit-exact vs the reference's execute() */
+};
+/* How the nest's cells map onto CTA tasks. */
+enum {
+    TM_SCHEDULE_FUSED = 0,    /* k loops sunk below the tile loops: one task per C tile, C in registers */
+    TM_SCHEDULE_FAITHFUL = 1  /* one task per nest cell in nest order; C round-trips per cell */
+};
+
+/* Replaces tilemul::ExecOptions (include/tilemul/exec.hpp:48-53). */
+typedef struct {
+    int32_t numerics;   /* TM_NUMERICS_* */
+    int32_t schedule;   /* TM_SCHEDULE_* */
+    int32_t split_k;    /* fused schedule: k splits per tile, deterministic reduction (1 = none, 0 = auto) */
+    int32_t ctas;       /* persistent grid size (0 = SMs x occupancy) */
+    int32_t tile;       /* CTA tile edge: 128 or 64 (0 = auto from the register tile) */
+} tm_exec_opts;
+
+typedef struct tm_plan tm_plan;
+
+/* --- errors ------------------------------------------------------------ */
+const char* tm_last_error(void);
+/* Rule ids of the last failure, one per line "rule:level:lhs:rhs". */
+const char* tm_last_rules(void);
+const char* tm_version(void);
+
+/* --- family descriptors (include/tilemul/descriptor.hpp) ---------------- */
+/* parse_name (:111-125): fills up to `cap` tiers, sets *count. */
+int tm_parse_name(const char* name, int allow_non_c_registers, tm_tier* tiers, int cap, int* count);
+/* make_descriptor (:68-107) from (level, resident) pairs, then format_name (:128-136). */
+int tm_compose(const int32_t* levels, const char* residents, int count, int allow_non_c_registers, char* name_out,
+               int name_cap, tm_tier* tiers, int cap, int* tier_count);
+/* validate_structure (:140-173) of an explicit tier list; returns #issues, rules in tm_last_rules(). */
+int tm_validate_structure(const tm_tier* tiers, int count, int allow_non_c_registers);
+/* skip_level (:177-195). */
+int tm_skip_level(const char* name, int level, char* name_out, int name_cap);
+/* select_algorithm (:206-218): writes 'A', 'B' or 'C'. */
+int tm_select_outer(int64_t m, int64_t n, int64_t k, int64_t outer_capacity, char* resident);
+
+/* --- blocksizes (include/tilemul/blocksizes.hpp) ------------------------- */
+/* derive_blocksizes (:243-425). Writes up to `cap` entries in (level, dim) order. */
+int tm_derive(const char* name, const tm_level* levels, int nlevels, int64_t m, int64_t n, int64_t k,
+              const tm_derive_opts* opts, const tm_blocksize* pinned, int npinned, tm_blocksize* out, int cap,
+              int* count);
+/* validate_blocksizes (:125-235): returns the number of violated rules (>= 0) or -status. */
+int tm_validate(const char* name, const tm_level* levels, int nlevels, int64_t m, int64_t n, int64_t k,
+                const tm_blocksize* bs, int nbs);
+/* The B200 memory hierarchy of the current device in FP64 elements:
+ * level 0 = CTA C tile (tile x tile), 1 = shared memory per block (opt-in),
+ * 2 = L2. Queried from the device; fails with 3 when no GPU is present. */
+int tm_gpu_hierarchy(int tile, tm_level* levels, int cap, int* count);
+
+/* --- plans (include/tilemul/plan.hpp) ----------------------------------- */
+/* build_plan (:90-108): validates and builds the nest; register level must be C. */
+int tm_plan_create(const char* name, const tm_level* levels, int nlevels, int64_t m, int64_t n, int64_t k,
+                   const tm_blocksize* bs, int nbs, tm_plan** plan);
+void tm_plan_destroy(tm_plan* plan);
+int tm_plan_loops(const tm_plan* plan, tm_loop* loops, int cap, int* count);
+int64_t tm_plan_cells(const tm_plan* plan);
+
+/* --- the I/O model (include/tilemul/costmodel.hpp) ----------------------- */
+/* multilevel_cost (:163-229): out[(h*3 + operand)*2 + {0 reads, 1 writes}], operands A,B,C. */
+int tm_plan_model(const tm_plan* plan, int64_t* out, int cap);
+/* multilevel_cost for any validated family member (no executable plan needed). */
+int tm_model(const char* name, int allow_non_c_registers, const tm_level* levels, int nlevels, int64_t m, int64_t n,
+             int64_t k, const tm_blocksize* bs, int nbs, int64_t* out, int cap);
+/* Number of levels of the hierarchy the plan was validated against. */
+int tm_plan_levels(const tm_plan* plan);
+/* io_lower_bound (:67-76). */
+int tm_io_lower_bound(int64_t m, int64_t n, int64_t k, int64_t fast_capacity, int64_t* reads, int64_t* writes);
+/* resident_cost (:85-100): out[operand*2 + {0,1}]. */
+int tm_resident_cost(char variant, int64_t m, int64_t n, int64_t k, int64_t b1, int64_t b2, int64_t* out);
+double tm_streaming_efficiency(char variant, int64_t b1, int64_t b2); /* :252-263 */
+double tm_goto_efficiency(int64_t k_c, int64_t n_c);                  /* :267-270 */
+double tm_roofline_bound(double intensity, double peak, double bandwidth); /* :278-284 */
+
+/* --- execution (include/tilemul/exec.hpp) ------------------------------ */
+/* execute (:94-138) on DEVICE buffers, asynchronous on `stream`:
+ * C(m x n, ldc) += A(m x k, lda) · B(k x n, ldb), column-major FP64. */
+int tm_execute(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+               const tm_exec_opts* opts, void* stream);
+/* execute on HOST buffers (the reference's own calling convention): copies
+ * A, B, C to the device, runs, copies C back; synchronous. Host memory may be
+ * pinned (fast path) or pageable. */
+int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts* opts);
+/* Number of CTA tasks and kernel launches the last tm_execute issued. */
+int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, int32_t* ctas);
+
+/* --- seeded device inputs ------------------------------------------------ */
+/* Counter-based uniform[-1,1) generator on the device (for operands too large
+ * to produce on the host): v = 2u - 1 with u from splitmix64(seed, index). */
+int tm_fill_uniform_device(double* x, int64_t count, uint64_t seed, uint64_t offset, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILEMUL_B200_H */

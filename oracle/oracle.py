@@ -1,0 +1,246 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes access to the CPU oracle.
+
+Two libraries, both checkers, never the thing measured or shipped:
+
+* ``oracle/liboracle.so`` — plain-C restatement of the reference's execution
+  path (``oracle/oracle.c``; exec.hpp:15-46, plan.hpp:61-84) and of the
+  seeded generator of ``tilemul run`` (tools/tilemul_main.cpp:236-242).
+* ``oracle/_ref/libtilemul_ref.so`` — the reference headers themselves,
+  compiled unmodified by ``oracle/Makefile`` (``ref_shim.cpp`` only adds a
+  C ABI). Present wherever it was built (this container, and the GPU box via
+  the gpurun snapshot).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (cpu_baseline
+leg and the ``--impl reference`` arm) may import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libtilemul_ref.so")
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+
+_lib = None
+_ref = None
+
+DIM_INDEX = {"m": 0, "n": 1, "k": 2}
+
+
+def build() -> None:
+    """Compile the oracle (and the reference, when its tree is present)."""
+    import subprocess
+
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        L = C.CDLL(ORACLE_SO)
+        L.or_fill_uniform.argtypes = [C.c_uint64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]
+        L.or_fill_uniform.restype = None
+        L.or_reference_gemm.argtypes = [C.c_int64] * 3 + [_dp, _dp, _dp]
+        L.or_reference_gemm.restype = None
+        L.or_execute.argtypes = [C.c_int64] * 3 + [_i32p, _i64p, C.c_int, C.c_int64, C.c_int64, _dp, _dp, _dp, C.c_int]
+        L.or_execute.restype = C.c_int64
+        L.or_entries.argtypes = [C.c_int64] * 3 + [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                                  _i64p, _i64p, C.c_int64, C.c_int, _dp, C.c_void_p]
+        L.or_entries.restype = None
+        L.or_abs_product.argtypes = [C.c_int64] * 3 + [_dp, _dp, _dp]
+        L.or_abs_product.restype = None
+        _lib = L
+    return _lib
+
+
+def have_ref() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    """The reference itself (oracle/_ref). Raises if it was never built."""
+    global _ref
+    if _ref is None:
+        if not have_ref():
+            raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference at build time)")
+        L = C.CDLL(REF_SO)
+        cp = C.c_char_p
+        L.ref_fill_uniform.argtypes = [C.c_uint64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]
+        L.ref_fill_uniform.restype = None
+        L.ref_mt19937_64.argtypes = [C.c_uint64, C.c_int64]
+        L.ref_mt19937_64.restype = C.c_uint64
+        L.ref_parse.argtypes = [cp, _i32p, C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        hier = [_i64p, _i32p, C.c_int, C.c_int64, C.c_int64, C.c_int64]
+        bs = [_i32p, C.c_char_p, _i64p, C.c_int]
+        L.ref_derive.argtypes = hier + [C.c_double, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double] + bs + [
+            _i32p, C.c_char_p, _i64p, C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        L.ref_derive.argtypes = [cp] + L.ref_derive.argtypes
+        L.ref_validate.argtypes = [cp] + hier + bs + [C.c_char_p, C.c_int]
+        L.ref_cost.argtypes = [cp] + hier + bs + [_i64p, C.c_char_p, C.c_int]
+        L.ref_nest.argtypes = [cp] + hier + bs + [_i32p, C.c_char_p, _i64p, _i32p, C.POINTER(C.c_int),
+                                                  C.POINTER(C.c_int64), C.c_char_p, C.c_int]
+        L.ref_execute.argtypes = [cp] + hier + bs + [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                                     C.POINTER(C.c_double), C.c_char_p, C.c_int]
+        L.ref_reference_gemm.argtypes = [C.c_int64] * 3 + [_dp, _dp, _dp]
+        L.ref_reference_gemm.restype = None
+        L.ref_micro_kernel.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                       C.c_int64, C.c_int64, C.c_int64]
+        L.ref_micro_kernel.restype = None
+        L.ref_io_lower_bound.argtypes = [C.c_int64] * 4 + [C.POINTER(C.c_int64)] * 2
+        L.ref_io_lower_bound.restype = None
+        L.ref_resident_cost.argtypes = [C.c_char] + [C.c_int64] * 5 + [_i64p]
+        L.ref_resident_cost.restype = None
+        L.ref_streaming_efficiency.argtypes = [C.c_char, C.c_int64, C.c_int64]
+        L.ref_streaming_efficiency.restype = C.c_double
+        L.ref_goto_efficiency.argtypes = [C.c_int64, C.c_int64]
+        L.ref_goto_efficiency.restype = C.c_double
+        L.ref_select.argtypes = [C.c_int64] * 4
+        L.ref_select.restype = C.c_char
+        _ref = L
+    return _ref
+
+
+# --------------------------------------------------------------------------
+# Restatement (liboracle.so)
+# --------------------------------------------------------------------------
+
+def fill_uniform(seed: int, shapes, lib_=None):
+    """Seeded matrices exactly as ``tilemul run`` fills them: one mt19937_64
+    stream, uniform(-1,1), operands in the given order (A, B[, C]).
+    ``shapes`` = list of (rows, cols); returns column-major float64 arrays
+    (flat, Fortran order)."""
+    arrs = [np.empty(r * c, dtype=np.float64) for r, c in shapes]
+    while len(arrs) < 3:
+        arrs.append(None)
+    L = lib_ or lib()
+    fn = L.or_fill_uniform if hasattr(L, "or_fill_uniform") else L.ref_fill_uniform
+    args = [C.c_uint64(seed)]
+    for a in arrs[:3]:
+        args += [a.ctypes.data if a is not None else None, C.c_int64(a.size if a is not None else 0)]
+    fn(*args)
+    return [a for a in arrs if a is not None]
+
+
+def reference_gemm(m, n, k, a, b, c):
+    """In place: c += a·b, naive i-j-p (exec.hpp:15-30)."""
+    lib().or_reference_gemm(m, n, k, a, b, c)
+
+
+def execute_nest(m, n, k, loops, mr, nr, a, b, c, fused=False) -> int:
+    """In place: the restated execute() over a nest given as [(dim, bs)]."""
+    dims = np.array([DIM_INDEX[d] for d, _ in loops], dtype=np.int32)
+    bsz = np.array([b for _, b in loops], dtype=np.int64)
+    return lib().or_execute(m, n, k, dims, bsz, len(loops), mr, nr, a, b, c, 1 if fused else 0)
+
+
+def entries(k, a, lda, b, ldb, c0, ldc, ii, jj, fused=False):
+    """Sequential-k values of sampled C entries plus (|A||B|)_ij for each."""
+    ii = np.ascontiguousarray(ii, dtype=np.int64)
+    jj = np.ascontiguousarray(jj, dtype=np.int64)
+    out = np.empty(ii.size, dtype=np.float64)
+    ab = np.empty(ii.size, dtype=np.float64)
+    lib().or_entries(0, 0, k, a.ctypes.data, lda, b.ctypes.data, ldb,
+                     c0.ctypes.data if c0 is not None else None, ldc, ii, jj, ii.size, 1 if fused else 0,
+                     out, ab.ctypes.data)
+    return out, ab
+
+
+def abs_product(m, n, k, a, b):
+    out = np.empty(m * n, dtype=np.float64)
+    lib().or_abs_product(m, n, k, np.abs(a), np.abs(b), out)
+    return out
+
+
+# --------------------------------------------------------------------------
+# The reference (oracle/_ref)
+# --------------------------------------------------------------------------
+
+def _hier_args(caps, inclusive=None):
+    caps = np.ascontiguousarray(caps, dtype=np.int64)
+    inc = np.ascontiguousarray(inclusive if inclusive is not None else [0] * caps.size, dtype=np.int32)
+    return caps, inc, caps.size
+
+
+def _bs_args(bs):
+    """bs: dict {(level, dim): value} or list of (level, dim, value)."""
+    items = sorted(bs.items()) if isinstance(bs, dict) else list(bs)
+    if isinstance(bs, dict):
+        items = [(lv, d, v) for (lv, d), v in items]
+    lvl = np.array([i[0] for i in items], dtype=np.int32)
+    dim = "".join(i[1] for i in items).encode()
+    val = np.array([i[2] for i in items], dtype=np.int64)
+    return lvl, dim, val, len(items)
+
+
+def ref_derive(name, caps, shape, slack=1.0 / 16.0, mr=4, nr=12, betas=(1.0, 1.0, 1.0), pinned=None,
+               inclusive=None):
+    L = ref()
+    lvl, dim, val, npin = _bs_args(pinned or {})
+    ol = np.zeros(64, dtype=np.int32)
+    od = C.create_string_buffer(64)
+    ov = np.zeros(64, dtype=np.int64)
+    no = C.c_int(0)
+    err = C.create_string_buffer(4096)
+    rc = L.ref_derive(name.encode(), *_hier_args(caps, inclusive), *shape, slack, mr, nr, *betas,
+                      lvl, dim, val, npin, ol, od, ov, C.byref(no), err, 4096)
+    if rc != 0:
+        return rc, err.value.decode()
+    return 0, {(int(ol[i]), od.raw[i:i + 1].decode()): int(ov[i]) for i in range(no.value)}
+
+
+def ref_validate(name, caps, shape, bs, inclusive=None):
+    L = ref()
+    err = C.create_string_buffer(1 << 16)
+    n = L.ref_validate(name.encode(), *_hier_args(caps, inclusive), *shape, *_bs_args(bs), err, 1 << 16)
+    rules = [ln.split(":") for ln in err.value.decode().splitlines() if ln]
+    return n, [(r[0], int(r[1]), int(r[2]), int(r[3])) for r in rules] if n > 0 else []
+
+
+def ref_cost(name, caps, shape, bs, inclusive=None):
+    L = ref()
+    caps_a = np.ascontiguousarray(caps, dtype=np.int64)
+    out = np.zeros(caps_a.size * 6, dtype=np.int64)
+    err = C.create_string_buffer(4096)
+    rc = L.ref_cost(name.encode(), *_hier_args(caps, inclusive), *shape, *_bs_args(bs), out, err, 4096)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    return out.reshape(caps_a.size, 3, 2)
+
+
+def ref_nest(name, caps, shape, bs, inclusive=None):
+    L = ref()
+    ol = np.zeros(64, dtype=np.int32)
+    od = C.create_string_buffer(64)
+    ob = np.zeros(64, dtype=np.int64)
+    oc = np.zeros(64, dtype=np.int32)
+    nl = C.c_int(0)
+    cells = C.c_int64(0)
+    err = C.create_string_buffer(4096)
+    rc = L.ref_nest(name.encode(), *_hier_args(caps, inclusive), *shape, *_bs_args(bs), ol, od, ob, oc,
+                    C.byref(nl), C.byref(cells), err, 4096)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    loops = [(int(ol[i]), od.raw[i:i + 1].decode(), int(ob[i]), bool(oc[i])) for i in range(nl.value)]
+    return loops, cells.value
+
+
+def ref_execute(name, caps, shape, bs, a, b, c, workers=1, parallel_loop=-1, packed=False, inclusive=None):
+    """In place on c (float64 column-major). Returns execute() seconds."""
+    L = ref()
+    secs = C.c_double(0)
+    err = C.create_string_buffer(4096)
+    rc = L.ref_execute(name.encode(), *_hier_args(caps, inclusive), *shape, *_bs_args(bs), a.ctypes.data,
+                       b.ctypes.data, c.ctypes.data, workers, parallel_loop, 1 if packed else 0, C.byref(secs),
+                       err, 4096)
+    if rc != 0:
+        raise ValueError(f"rc={rc}: {err.value.decode()}")
+    return secs.value

@@ -1,0 +1,560 @@
+// C ABI (include/tilemul_b200.h) over the host library and the sm_100a task
+// kernels, plus the lowering of a loop nest onto CTA tasks.
+//
+// Lowering (the blocked-loop driver, reference plan.hpp:61-84 +
+// exec.hpp:94-138, re-targeted): a task is one C region x k range run by one
+// CTA with its accumulators in registers. Two schedules:
+//   fused    — every k loop of the nest is sunk below its m/n loops, so each
+//              register-level C block is visited once, in the order of its
+//              first appearance in the nest (the m/n loops above it become the
+//              CTA raster: the L2-level plan sets which tiles share a wave).
+//              Optional split-k adds a deterministic slice reduction.
+//   faithful — one task per nest cell, in nest order; cells of the same C
+//              block run in ascending k (per-region progress counters), so
+//              the C block round-trips to memory per cell exactly as the
+//              reference's micro-kernel does.
+// Either way every C entry is accumulated in ascending k from its incoming
+// value, which is what makes the result independent of the schedule.
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/tilemul_b200.h"
+#include "host/mmm.hpp"
+#include "kernels/gpu.hpp"
+
+using namespace mmm;
+
+namespace {
+
+thread_local std::string g_error;
+thread_local std::string g_rules;
+
+void record(const Failure& f) {
+    g_error = f.what();
+    g_rules.clear();
+    for (const auto& v : f.issues)
+        g_rules += v.rule + ":" + std::to_string(v.level) + ":" + std::to_string(v.lhs) + ":" + std::to_string(v.rhs) + "\n";
+    if (f.issues.empty() && !f.rule.empty()) g_rules = f.rule + ":-1:0:0\n";
+}
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        g_error.clear();
+        g_rules.clear();
+        f();
+        return kOk;
+    } catch (const Failure& e) {
+        record(e);
+        return e.status;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return kUsage;
+    }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Failure(kDevice, "", std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+Hierarchy hierarchy_from(const tm_level* levels, int n) {
+    if (n < 1 || levels == nullptr) fail_usage("hierarchy needs at least one level");
+    std::vector<MemLevel> lv;
+    for (int i = 0; i < n; ++i)
+        lv.push_back({levels[i].capacity_elements, levels[i].granularity < 1 ? 1 : levels[i].granularity,
+                      levels[i].inclusive != 0, levels[i].write_allocate != 0, levels[i].write_back != 0});
+    return make_hierarchy(std::move(lv));
+}
+
+Blocks blocks_from(const tm_blocksize* bs, int n) {
+    Blocks b;
+    for (int i = 0; i < n; ++i) b.put(bs[i].level, dim_of_char(bs[i].dim), bs[i].value);
+    return b;
+}
+
+void put_tiers(const Family& f, tm_tier* tiers, int cap, int* count) {
+    if (count) *count = static_cast<int>(f.tiers.size());
+    if (tiers == nullptr) return;
+    if (static_cast<int>(f.tiers.size()) > cap) fail_usage("tier buffer too small");
+    for (std::size_t i = 0; i < f.tiers.size(); ++i)
+        tiers[i] = tm_tier{f.tiers[i].level, opnd_char(f.tiers[i].resident), dim_char(f.tiers[i].outer),
+                           dim_char(f.tiers[i].inner)};
+}
+
+void put_name(const std::string& s, char* out, int cap) {
+    if (out == nullptr) return;
+    if (static_cast<int>(s.size()) + 1 > cap) fail_usage("name buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+}
+
+// ------------------------------------------------------------- lowering
+
+struct Schedule {
+    gpu::Kernel kernel = gpu::kDmma128;
+    bool vec16 = false;
+    int grid = 1;
+    int slices = 1;          // split-k slices (fused)
+    int regions = 0;         // progress counters (faithful)
+    std::vector<gpu::Task> host_tasks;
+    gpu::Task* tasks = nullptr;
+    int32_t* progress = nullptr;
+    double* work = nullptr;
+    int64_t work_ld = 0, work_slice = 0;
+    int device = -1;
+    ~Schedule() {
+        if (tasks) cudaFree(tasks);
+        if (progress) cudaFree(progress);
+        if (work) cudaFree(work);
+    }
+};
+
+struct Key {
+    int schedule, kernel, split, ctas;
+    bool vec16;
+    bool operator<(const Key& o) const {
+        return std::tie(schedule, kernel, split, ctas, vec16) < std::tie(o.schedule, o.kernel, o.split, o.ctas, o.vec16);
+    }
+};
+
+}  // namespace
+
+struct tm_plan {
+    Nest nest;
+    Hierarchy hier;
+    std::map<Key, std::unique_ptr<Schedule>> schedules;
+    std::mutex mu;
+    // host-buffer execution
+    double *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    cudaStream_t host_stream = nullptr;
+    int64_t last_tasks = 0;
+    int32_t last_launches = 0, last_ctas = 0;
+    ~tm_plan() {
+        if (dA) cudaFree(dA);
+        if (dB) cudaFree(dB);
+        if (dC) cudaFree(dC);
+        if (host_stream) cudaStreamDestroy(host_stream);
+    }
+};
+
+namespace {
+
+int sm_count() {
+    int dev = 0, sms = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    return sms;
+}
+
+gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o) {
+    const bool small_tile = o.tile == 64 || (o.tile == 0 && (nest.m_r < 128 || nest.n_r < 128));
+    if (o.tile != 0 && o.tile != 64 && o.tile != 128) fail_usage("tile must be 0, 64 or 128");
+    switch (o.numerics) {
+        case TM_NUMERICS_DMMA: return small_tile ? gpu::kDmma64 : gpu::kDmma128;
+        case TM_NUMERICS_FMA: return small_tile ? gpu::kFma64 : gpu::kFma128;
+        case TM_NUMERICS_EXACT:
+            if (o.tile == 128) fail_usage("exact numerics run on the 64x64 tile only");
+            return gpu::kExact64;
+        default: fail_usage("unknown numerics");
+    }
+}
+
+// Splits one C region into kernel tiles, n outer / m inner (the register
+// plan's own loop order, C0 = n then m).
+template <typename F>
+void for_each_subtile(i64 i0, i64 m, i64 j0, i64 n, int tm, int tn, F&& f) {
+    for (i64 jj = 0; jj < n; jj += tn)
+        for (i64 ii = 0; ii < m; ii += tm) f(i0 + ii, std::min<i64>(tm, m - ii), j0 + jj, std::min<i64>(tn, n - jj));
+}
+
+void check_i32(i64 v, const char* what) {
+    if (v > INT32_MAX) fail_usage(std::string(what) + " exceeds the 32-bit task range");
+}
+
+std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel) {
+    auto s = std::make_unique<Schedule>();
+    s->kernel = kernel;
+    gpu::KernelInfo info{};
+    cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
+    const int slots = sm_count() * std::max(1, info.ctas_per_sm);
+    const Extents& e = nest.ext;
+    check_i32(e.m, "m");
+    check_i32(e.n, "n");
+    check_i32(e.k, "k");
+    auto& T = s->host_tasks;
+
+    if (o.schedule == TM_SCHEDULE_FUSED) {
+        // First-appearance order of the register-level C blocks = the walk of
+        // the nest with its k loops removed.
+        Nest mn = nest;
+        mn.loops.clear();
+        for (const auto& L : nest.loops)
+            if (L.dim != kK) mn.loops.push_back(L);
+        std::vector<std::array<i64, 4>> tiles;
+        mn.walk([&](const Cell& c) {
+            for_each_subtile(c.i0, c.m, c.j0, c.n, info.tile_m, info.tile_n,
+                             [&](i64 i0, i64 m, i64 j0, i64 n) { tiles.push_back({i0, m, j0, n}); });
+        });
+        int split = o.split_k;
+        if (split == 0) {  // auto: fill the machine when C has too few tiles
+            split = 1;
+            const i64 nt = static_cast<i64>(tiles.size());
+            if (nt * 2 <= slots) split = static_cast<int>(std::min<i64>(slots / nt, std::max<i64>(1, e.k / 1024)));
+        }
+        split = std::max(1, std::min<int>(split, static_cast<int>(cdiv(e.k, 16))));
+        s->slices = split;
+        // k ranges aligned to the 16-deep slab
+        const i64 per = cdiv(cdiv(e.k, split), 16) * 16;
+        for (const auto& t : tiles)
+            for (int q = 0; q < split; ++q) {
+                const i64 p0 = q * per;
+                if (p0 >= e.k) break;
+                gpu::Task tk{};
+                tk.i0 = static_cast<int32_t>(t[0]);
+                tk.m = static_cast<int32_t>(t[1]);
+                tk.j0 = static_cast<int32_t>(t[2]);
+                tk.n = static_cast<int32_t>(t[3]);
+                tk.p0 = static_cast<int32_t>(p0);
+                tk.k = static_cast<int32_t>(std::min(per, e.k - p0));
+                tk.tile = -1;
+                tk.seq = 0;
+                tk.slice = split > 1 ? q : -1;
+                tk.from_c = q == 0 ? 1 : 0;
+                T.push_back(tk);
+            }
+        if (split > 1) {
+            // slices beyond the last non-empty one never get written
+            const int used = static_cast<int>(cdiv(e.k, per));
+            s->slices = used;
+            s->work_ld = e.m;
+            s->work_slice = e.m * e.n;
+            cuda_check(cudaMalloc(&s->work, sizeof(double) * static_cast<std::size_t>(s->work_slice) * used),
+                       "cudaMalloc(split-k workspace)");
+            if (used == 1)
+                for (auto& tk : T) tk.slice = -1;
+            if (used == 1) s->slices = 1;
+        }
+    } else if (o.schedule == TM_SCHEDULE_FAITHFUL) {
+        const i64 cells = nest.cells();
+        if (cells > 64LL * 1000 * 1000) fail_usage("faithful schedule limited to 64M cells; use the fused schedule");
+        std::unordered_map<i64, std::pair<int32_t, int32_t>> regions;  // key -> (id, next seq)
+        nest.walk([&](const Cell& c) {
+            for_each_subtile(c.i0, c.m, c.j0, c.n, info.tile_m, info.tile_n, [&](i64 i0, i64 m, i64 j0, i64 n) {
+                const i64 key = i0 * (e.n + 1) + j0;
+                auto it = regions.find(key);
+                if (it == regions.end()) it = regions.emplace(key, std::make_pair(static_cast<int32_t>(regions.size()), 0)).first;
+                gpu::Task tk{};
+                tk.i0 = static_cast<int32_t>(i0);
+                tk.m = static_cast<int32_t>(m);
+                tk.j0 = static_cast<int32_t>(j0);
+                tk.n = static_cast<int32_t>(n);
+                tk.p0 = static_cast<int32_t>(c.p0);
+                tk.k = static_cast<int32_t>(c.k);
+                tk.tile = it->second.first;
+                tk.seq = it->second.second++;
+                tk.slice = -1;
+                tk.from_c = 1;
+                T.push_back(tk);
+            });
+        });
+        s->regions = static_cast<int>(regions.size());
+        cuda_check(cudaMalloc(&s->progress, sizeof(int32_t) * static_cast<std::size_t>(std::max(1, s->regions))),
+                   "cudaMalloc(progress)");
+    } else {
+        fail_usage("unknown schedule");
+    }
+    if (T.size() > static_cast<std::size_t>(INT32_MAX)) fail_usage("too many tasks");
+    // Persistent grid: every CTA must be co-resident for the faithful
+    // schedule's waits to make progress.
+    int grid = o.ctas > 0 ? std::min(o.ctas, slots) : slots;
+    s->grid = std::max(1, std::min<int>(grid, static_cast<int>(T.size())));
+    cuda_check(cudaGetDevice(&s->device), "cudaGetDevice");
+    cuda_check(cudaMalloc(&s->tasks, sizeof(gpu::Task) * std::max<std::size_t>(1, T.size())), "cudaMalloc(tasks)");
+    cuda_check(cudaMemcpy(s->tasks, T.data(), sizeof(gpu::Task) * T.size(), cudaMemcpyHostToDevice), "upload tasks");
+    return s;
+}
+
+bool origins_even(const std::vector<gpu::Task>& T) {
+    for (const auto& t : T)
+        if ((t.i0 | t.p0) & 1) return false;
+    return true;
+}
+
+void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+         const tm_exec_opts* opts, cudaStream_t stream) {
+    const Extents& e = plan->nest.ext;
+    if (!A || !B || !C) fail_usage("null operand pointer");
+    if (lda < e.m || ldb < e.k || ldc < e.m) fail_usage("leading dimension smaller than the operand's row count");
+    tm_exec_opts o{};
+    if (opts) o = *opts;
+    const gpu::Kernel kernel = pick_kernel(plan->nest, o);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    Key key{o.schedule, kernel, o.schedule == TM_SCHEDULE_FUSED ? o.split_k : 0, o.ctas, false};
+    auto& slot = plan->schedules[key];
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (!slot || slot->device != dev) slot = lower(plan->nest, o, kernel);
+    Schedule& s = *slot;
+    const bool vec16 = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(B) % 16 == 0) && origins_even(s.host_tasks);
+    if (s.regions > 0)
+        cuda_check(cudaMemsetAsync(s.progress, 0, sizeof(int32_t) * static_cast<std::size_t>(s.regions), stream),
+                   "reset progress");
+    gpu::Args a{A, lda, B, ldb, C, ldc, s.tasks, static_cast<int32_t>(s.host_tasks.size()), s.progress, s.work,
+                s.work_ld, s.work_slice};
+    cuda_check(gpu::launch(s.kernel, vec16, a, s.grid, stream), "task kernel launch");
+    int launches = 1;
+    if (s.slices > 1) {
+        cuda_check(gpu::launch_reduce(C, ldc, s.work, s.work_ld, s.work_slice, s.slices, e.m, e.n, stream),
+                   "split-k reduce launch");
+        ++launches;
+    }
+    plan->last_tasks = static_cast<int64_t>(s.host_tasks.size());
+    plan->last_launches = launches;
+    plan->last_ctas = s.grid;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tm_last_error(void) { return g_error.c_str(); }
+const char* tm_last_rules(void) { return g_rules.c_str(); }
+const char* tm_version(void) { return "tilemul_b200 0.1 (sm_100a)"; }
+
+int tm_parse_name(const char* name, int allow_non_c, tm_tier* tiers, int cap, int* count) {
+    return guard([&] {
+        if (!name) fail_usage("null name");
+        put_tiers(family_from_name(name, allow_non_c != 0), tiers, cap, count);
+    });
+}
+
+int tm_compose(const int32_t* levels, const char* residents, int count, int allow_non_c, char* name_out, int name_cap,
+               tm_tier* tiers, int cap, int* tier_count) {
+    return guard([&] {
+        std::vector<std::pair<int, Opnd>> r;
+        for (int i = 0; i < count; ++i) r.emplace_back(levels[i], opnd_of_char(residents[i]));
+        Family f = compose(r, allow_non_c != 0);
+        put_name(family_name(f), name_out, name_cap);
+        put_tiers(f, tiers, cap, tier_count);
+    });
+}
+
+int tm_validate_structure(const tm_tier* tiers, int count, int allow_non_c) {
+    int n = 0;
+    int rc = guard([&] {
+        Family f;
+        f.free_registers = allow_non_c != 0;
+        for (int i = 0; i < count; ++i)
+            f.tiers.push_back(Tier{tiers[i].level, opnd_of_char(tiers[i].resident), dim_of_char(tiers[i].outer_dim),
+                                   dim_of_char(tiers[i].inner_dim)});
+        auto issues = structure_issues(f);
+        n = static_cast<int>(issues.size());
+        for (const auto& v : issues)
+            g_rules += v.rule + ":" + std::to_string(v.level) + ":" + std::to_string(v.lhs) + ":" + std::to_string(v.rhs) + "\n";
+    });
+    return rc == kOk ? n : -rc;
+}
+
+int tm_skip_level(const char* name, int level, char* name_out, int name_cap) {
+    return guard([&] { put_name(family_name(without_level(family_from_name(name), level)), name_out, name_cap); });
+}
+
+int tm_select_outer(int64_t m, int64_t n, int64_t k, int64_t cap, char* resident) {
+    return guard([&] { *resident = opnd_char(outer_resident_for(make_extents(m, n, k), cap)); });
+}
+
+int tm_derive(const char* name, const tm_level* levels, int nlevels, int64_t m, int64_t n, int64_t k,
+              const tm_derive_opts* opts, const tm_blocksize* pinned, int npinned, tm_blocksize* out, int cap,
+              int* count) {
+    return guard([&] {
+        DeriveOpts d;
+        Weights w;
+        if (opts) {
+            d.slack = opts->slack;
+            d.m_r = opts->m_r;
+            d.n_r = opts->n_r;
+            w = Weights{opts->beta_a, opts->beta_b, opts->beta_c};
+        }
+        Blocks bs = derive(family_from_name(name), hierarchy_from(levels, nlevels), make_extents(m, n, k), w, d,
+                           blocks_from(pinned, npinned));
+        auto ent = bs.entries();
+        if (count) *count = static_cast<int>(ent.size());
+        if (static_cast<int>(ent.size()) > cap) fail_usage("blocksize buffer too small");
+        for (std::size_t i = 0; i < ent.size(); ++i)
+            out[i] = tm_blocksize{std::get<0>(ent[i]), dim_char(std::get<1>(ent[i])), std::get<2>(ent[i])};
+    });
+}
+
+int tm_validate(const char* name, const tm_level* levels, int nlevels, int64_t m, int64_t n, int64_t k,
+                const tm_blocksize* bs, int nbs) {
+    int count = 0;
+    int rc = guard([&] {
+        (void)make_extents(m, n, k);
+        auto issues = fit_issues(family_from_name(name), blocks_from(bs, nbs), hierarchy_from(levels, nlevels));
+        count = static_cast<int>(issues.size());
+        for (const auto& v : issues)
+            g_rules += v.rule + ":" + std::to_string(v.level) + ":" + std::to_string(v.lhs) + ":" + std::to_string(v.rhs) + "\n";
+    });
+    return rc == kOk ? count : -rc;
+}
+
+int tm_gpu_hierarchy(int tile, tm_level* levels, int cap, int* count) {
+    return guard([&] {
+        if (tile != 64 && tile != 128) fail_usage("tile must be 64 or 128");
+        if (cap < 3) fail_usage("level buffer too small");
+        int dev = 0, smem = 0, l2 = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        cuda_check(cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem attr");
+        cuda_check(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev), "l2 attr");
+        levels[0] = tm_level{static_cast<int64_t>(tile) * tile, 1, 0, 1, 1};
+        levels[1] = tm_level{smem / 8, 1, 0, 1, 1};
+        levels[2] = tm_level{l2 / 8, 1, 0, 1, 1};
+        if (count) *count = 3;
+    });
+}
+
+int tm_plan_create(const char* name, const tm_level* levels, int nlevels, int64_t m, int64_t n, int64_t k,
+                   const tm_blocksize* bs, int nbs, tm_plan** plan) {
+    return guard([&] {
+        if (!plan) fail_usage("null plan out-pointer");
+        auto p = std::make_unique<tm_plan>();
+        p->hier = hierarchy_from(levels, nlevels);
+        p->nest = build_nest(family_from_name(name), blocks_from(bs, nbs), p->hier, make_extents(m, n, k));
+        *plan = p.release();
+    });
+}
+
+void tm_plan_destroy(tm_plan* plan) { delete plan; }
+
+int tm_plan_loops(const tm_plan* plan, tm_loop* loops, int cap, int* count) {
+    return guard([&] {
+        const auto& L = plan->nest.loops;
+        if (count) *count = static_cast<int>(L.size());
+        if (static_cast<int>(L.size()) > cap) fail_usage("loop buffer too small");
+        for (std::size_t i = 0; i < L.size(); ++i)
+            loops[i] = tm_loop{L[i].level, dim_char(L[i].dim), L[i].size, L[i].cap ? 1 : 0};
+    });
+}
+
+int64_t tm_plan_cells(const tm_plan* plan) { return plan ? plan->nest.cells() : -1; }
+
+int tm_plan_model(const tm_plan* plan, int64_t* out, int cap) {
+    return guard([&] {
+        if (!plan) fail_usage("null plan");
+        IoModel r = level_io(plan->nest.family, plan->nest.blocks, plan->hier, plan->nest.ext);
+        if (static_cast<int>(r.levels.size()) * 6 > cap) fail_usage("model buffer too small");
+        for (const auto& lf : r.levels)
+            for (int o = 0; o < 3; ++o) {
+                out[(lf.level * 3 + o) * 2] = lf.op[static_cast<std::size_t>(o)].reads;
+                out[(lf.level * 3 + o) * 2 + 1] = lf.op[static_cast<std::size_t>(o)].writes;
+            }
+    });
+}
+
+int tm_plan_levels(const tm_plan* plan) { return plan ? plan->hier.size() : -1; }
+
+int tm_model(const char* name, int allow_non_c, const tm_level* levels, int nlevels, int64_t m, int64_t n, int64_t k,
+             const tm_blocksize* bs, int nbs, int64_t* out, int cap) {
+    return guard([&] {
+        IoModel r = level_io(family_from_name(name, allow_non_c != 0), blocks_from(bs, nbs),
+                             hierarchy_from(levels, nlevels), make_extents(m, n, k));
+        if (static_cast<int>(r.levels.size()) * 6 > cap) fail_usage("model buffer too small");
+        for (const auto& lf : r.levels)
+            for (int o = 0; o < 3; ++o) {
+                out[(lf.level * 3 + o) * 2] = lf.op[static_cast<std::size_t>(o)].reads;
+                out[(lf.level * 3 + o) * 2 + 1] = lf.op[static_cast<std::size_t>(o)].writes;
+            }
+    });
+}
+
+int tm_io_lower_bound(int64_t m, int64_t n, int64_t k, int64_t M, int64_t* reads, int64_t* writes) {
+    return guard([&] {
+        Flow f = lower_bound_io(make_extents(m, n, k), M);
+        *reads = f.reads;
+        *writes = f.writes;
+    });
+}
+
+int tm_resident_cost(char variant, int64_t m, int64_t n, int64_t k, int64_t b1, int64_t b2, int64_t* out) {
+    return guard([&] {
+        LevelFlow t = resident_io(opnd_of_char(variant), make_extents(m, n, k), b1, b2);
+        for (int o = 0; o < 3; ++o) {
+            out[o * 2] = t.op[static_cast<std::size_t>(o)].reads;
+            out[o * 2 + 1] = t.op[static_cast<std::size_t>(o)].writes;
+        }
+    });
+}
+
+double tm_streaming_efficiency(char variant, int64_t b1, int64_t b2) {
+    double r = -1;
+    guard([&] { r = streaming_flops_per_element(opnd_of_char(variant), b1, b2); });
+    return r;
+}
+
+double tm_goto_efficiency(int64_t k_c, int64_t n_c) {
+    double r = -1;
+    guard([&] { r = goto_flops_per_element(k_c, n_c); });
+    return r;
+}
+
+double tm_roofline_bound(double intensity, double peak, double bandwidth) {
+    double r = -1;
+    guard([&] { r = roofline(intensity, peak, bandwidth); });
+    return r;
+}
+
+int tm_execute(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+               const tm_exec_opts* opts, void* stream) {
+    return guard([&] {
+        if (!plan) fail_usage("null plan");
+        run(plan, A, lda, B, ldb, C, ldc, opts, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts* opts) {
+    return guard([&] {
+        if (!plan) fail_usage("null plan");
+        if (!A || !B || !C) fail_usage("null operand pointer");
+        const Extents& e = plan->nest.ext;
+        const std::size_t na = static_cast<std::size_t>(e.m * e.k), nb = static_cast<std::size_t>(e.k * e.n),
+                          nc = static_cast<std::size_t>(e.m * e.n);
+        if (!plan->host_stream)
+            cuda_check(cudaStreamCreateWithFlags(&plan->host_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (!plan->dA) {
+            cuda_check(cudaMalloc(&plan->dA, na * sizeof(double)), "cudaMalloc(A)");
+            cuda_check(cudaMalloc(&plan->dB, nb * sizeof(double)), "cudaMalloc(B)");
+            cuda_check(cudaMalloc(&plan->dC, nc * sizeof(double)), "cudaMalloc(C)");
+        }
+        cudaStream_t st = plan->host_stream;
+        cuda_check(cudaMemcpyAsync(plan->dA, A, na * sizeof(double), cudaMemcpyHostToDevice, st), "H2D A");
+        cuda_check(cudaMemcpyAsync(plan->dB, B, nb * sizeof(double), cudaMemcpyHostToDevice, st), "H2D B");
+        cuda_check(cudaMemcpyAsync(plan->dC, C, nc * sizeof(double), cudaMemcpyHostToDevice, st), "H2D C");
+        run(plan, plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, opts, st);
+        cuda_check(cudaMemcpyAsync(C, plan->dC, nc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H C");
+        cuda_check(cudaStreamSynchronize(st), "execute_host sync");
+    });
+}
+
+int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, int32_t* ctas) {
+    return guard([&] {
+        if (tasks) *tasks = plan->last_tasks;
+        if (launches) *launches = plan->last_launches;
+        if (ctas) *ctas = plan->last_ctas;
+    });
+}
+
+int tm_fill_uniform_device(double* x, int64_t count, uint64_t seed, uint64_t offset, void* stream) {
+    return guard([&] {
+        cuda_check(gpu::launch_fill(x, count, seed, offset, static_cast<cudaStream_t>(stream)), "fill launch");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,431 @@
+// FP64 C += A·B task kernels for sm_100a (B200).
+//
+// A launch processes a list of CTA tasks (gpu.hpp) with a persistent grid.
+// Every task is one C region accumulated in ascending k from its incoming
+// value — the reference's micro-kernel cell (exec.hpp:35-46) at CTA
+// granularity. A and B k-slabs are staged global->shared through a
+// multi-stage cp.async ring (the SMEM level of the family member); the C
+// region lives in registers for the whole task (the register level).
+//
+// Numerics variants:
+//   k_dmma  — FP64 tensor pipe (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4),
+//             the fast path (B200: 64 FP64 FMA/clk/SM on either pipe; the
+//             DMMA path leaves the issue slots free for the staging loads).
+//   k_simt<FMA>   — one DFMA per (entry, k): bit-exact against a sequential
+//                   fma restatement of the reference cell.
+//   k_simt<EXACT> — DMUL then DADD per (entry, k): bit-exact against the
+//                   reference's own execute() (built -O2, no FMA contraction).
+#include <cstdint>
+
+#include "gpu.hpp"
+
+namespace mmm {
+namespace gpu {
+namespace {
+
+constexpr int kBK = 16;  // k-slab depth per pipeline stage
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp16(double* dst, const double* src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(dst)), "l"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp8(double* dst, const double* src, int bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_addr(dst)), "l"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// ---- ordering between tasks on the same C region (faithful schedule) ----
+__device__ __forceinline__ void wait_turn(const Args& a, const Task& t) {
+    if (t.tile < 0 || t.seq <= 0) return;
+    if (threadIdx.x == 0) {
+        int v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(a.progress + t.tile) : "memory");
+            if (v >= t.seq) break;
+            __nanosleep(100);
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void signal_done(const Args& a, const Task& t) {
+    if (t.tile < 0) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(a.progress + t.tile), "r"(t.seq + 1) : "memory");
+    }
+}
+
+// Where a task reads its starting value and writes its result.
+struct Dest {
+    const double* src;  // nullptr: start from zero
+    double* dst;
+    int64_t ld_src, ld_dst;
+};
+__device__ __forceinline__ Dest resolve(const Args& a, const Task& t) {
+    Dest d;
+    if (t.slice < 0) {
+        d.src = a.C;
+        d.dst = a.C;
+        d.ld_src = d.ld_dst = a.ldc;
+    } else {
+        d.src = t.from_c ? a.C : nullptr;
+        d.ld_src = a.ldc;
+        d.dst = a.work + static_cast<int64_t>(t.slice) * a.work_slice;
+        d.ld_dst = a.work_ld;
+    }
+    return d;
+}
+
+// ---- shared-memory geometry ----
+// As[k][m] (row stride BM+4 doubles: the 4-double pad puts the four k rows a
+// DMMA A-fragment touches 8 banks apart -> 2 wavefronts per 64-bit load, the
+// minimum). Bs[n][k] (stride BK+4, same argument for the B-fragment).
+// The SIMT kernels keep B transposed, Bt[k][n], so a thread's n-run is
+// contiguous.
+template <int BM, int BN, bool BT>
+struct Geo {
+    static constexpr int LDA = BM + 4;
+    static constexpr int LDB = BT ? BN + 4 : kBK + 4;
+    static constexpr int A_ELEMS = kBK * LDA;
+    static constexpr int B_ELEMS = BT ? kBK * LDB : BN * LDB;
+    static constexpr int STAGE = A_ELEMS + B_ELEMS;
+};
+
+// One k-slab [p, p+BK) of the task's A rows and B columns into one stage;
+// out-of-range elements are zero-filled (cp.async src-size < cp-size).
+template <int BM, int BN, int NT, bool V16, bool BT>
+__device__ __forceinline__ void load_slab(double* As, double* Bs, const Args& a, const Task& t, int p) {
+    using G = Geo<BM, BN, BT>;
+    const int tid = threadIdx.x;
+    const int klim = t.p0 + t.k - p;
+    const double* Ab = a.A + static_cast<int64_t>(t.i0) + static_cast<int64_t>(p) * a.lda;
+    const double* Bb = a.B + static_cast<int64_t>(p) + static_cast<int64_t>(t.j0) * a.ldb;
+    if constexpr (V16) {
+#pragma unroll
+        for (int q = tid; q < BM * kBK / 2; q += NT) {
+            const int c = q / (BM / 2), r = (q % (BM / 2)) * 2;
+            const int v = c < klim ? min(max(t.m - r, 0), 2) : 0;
+            cp16(As + c * G::LDA + r, v ? Ab + r + static_cast<int64_t>(c) * a.lda : a.A, v * 8);
+        }
+    } else {
+#pragma unroll 4
+        for (int q = tid; q < BM * kBK; q += NT) {
+            const int c = q / BM, r = q % BM;
+            const bool v = c < klim && r < t.m;
+            cp8(As + c * G::LDA + r, v ? Ab + r + static_cast<int64_t>(c) * a.lda : a.A, v ? 8 : 0);
+        }
+    }
+    if constexpr (BT) {
+        // Bt[k][n]: consecutive threads walk k down one B column (coalesced).
+#pragma unroll 4
+        for (int q = tid; q < BN * kBK; q += NT) {
+            const int n = q / kBK, c = q % kBK;
+            const bool v = c < klim && n < t.n;
+            cp8(Bs + c * G::LDB + n, v ? Bb + c + static_cast<int64_t>(n) * a.ldb : a.B, v ? 8 : 0);
+        }
+    } else if constexpr (V16) {
+#pragma unroll
+        for (int q = tid; q < BN * kBK / 2; q += NT) {
+            const int n = q / (kBK / 2), c = (q % (kBK / 2)) * 2;
+            const int v = n < t.n ? min(max(klim - c, 0), 2) : 0;
+            cp16(Bs + n * G::LDB + c, v ? Bb + c + static_cast<int64_t>(n) * a.ldb : a.B, v * 8);
+        }
+    } else {
+#pragma unroll 4
+        for (int q = tid; q < BN * kBK; q += NT) {
+            const int n = q / kBK, c = q % kBK;
+            const bool v = c < klim && n < t.n;
+            cp8(Bs + n * G::LDB + c, v ? Bb + c + static_cast<int64_t>(n) * a.ldb : a.B, v ? 8 : 0);
+        }
+    }
+}
+
+// ============================== DMMA kernel ==============================
+template <int BM, int BN, int WM, int WN, int STAGES, bool V16>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) {
+    constexpr int NWM = BM / WM, NT = (BM / WM) * (BN / WN) * 32;
+    constexpr int FM = WM / 8, FN = WN / 8;
+    using G = Geo<BM, BN, false>;
+    extern __shared__ __align__(128) double smem[];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, tq = lane & 3;
+    const int wm0 = (warp % NWM) * WM, wn0 = (warp / NWM) * WN;
+
+    for (int ti = blockIdx.x; ti < a.ntasks; ti += gridDim.x) {
+        const Task t = a.tasks[ti];
+        wait_turn(a, t);
+        const int nk = (t.k + kBK - 1) / kBK;
+#pragma unroll
+        for (int s = 0; s < STAGES - 1; ++s) {
+            if (s < nk) load_slab<BM, BN, NT, V16, false>(smem + s * G::STAGE, smem + s * G::STAGE + G::A_ELEMS, a, t,
+                                                         t.p0 + s * kBK);
+            cp_commit();
+        }
+
+        const Dest d = resolve(a, t);
+        double acc[FM][FN][2];
+#pragma unroll
+        for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int r = wm0 + mi * 8 + g, c = wn0 + ni * 8 + 2 * tq + e;
+                    acc[mi][ni][e] = (d.src && r < t.m && c < t.n)
+                                         ? __ldcg(d.src + (t.i0 + r) + static_cast<int64_t>(t.j0 + c) * d.ld_src)
+                                         : 0.0;
+                }
+
+        for (int s = 0; s < nk; ++s) {
+            cp_wait<STAGES - 2>();
+            __syncthreads();
+            const int nx = s + STAGES - 1;
+            if (nx < nk) {
+                double* st = smem + (nx % STAGES) * G::STAGE;
+                load_slab<BM, BN, NT, V16, false>(st, st + G::A_ELEMS, a, t, t.p0 + nx * kBK);
+            }
+            cp_commit();
+            const double* As = smem + (s % STAGES) * G::STAGE;
+            const double* Bs = As + G::A_ELEMS;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 4; ++kk) {
+                double af[FM], bf[FN];
+#pragma unroll
+                for (int mi = 0; mi < FM; ++mi) af[mi] = As[(kk * 4 + tq) * G::LDA + wm0 + mi * 8 + g];
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni) bf[ni] = Bs[(wn0 + ni * 8 + g) * G::LDB + kk * 4 + tq];
+#pragma unroll
+                for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < FN; ++ni) dmma884(acc[mi][ni], af[mi], bf[ni]);
+            }
+        }
+        cp_wait<0>();
+        __syncthreads();
+
+        const int64_t di = t.i0, dj = t.j0;
+#pragma unroll
+        for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int r = wm0 + mi * 8 + g, c = wn0 + ni * 8 + 2 * tq + e;
+                    if (r < t.m && c < t.n) d.dst[(di + r) + (dj + c) * d.ld_dst] = acc[mi][ni][e];
+                }
+        signal_done(a, t);
+    }
+}
+
+// ============================== SIMT kernels =============================
+// Thread (tx, ty) owns rows ty*TM.., columns tx*TN.. of the CTA tile; each
+// entry accumulates one k at a time, in ascending order, only over k that
+// exist (no zero-padded steps), so results are bit-reproducible on the CPU.
+template <int BM, int BN, int TM, int TN, int STAGES, bool EXACT>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN)) k_simt(Args a) {
+    constexpr int NTX = BN / TN, NT = (BM / TM) * (BN / TN);
+    using G = Geo<BM, BN, true>;
+    extern __shared__ __align__(128) double smem[];
+    const int tx = threadIdx.x % NTX, ty = threadIdx.x / NTX;
+    const int r0 = ty * TM, c0 = tx * TN;
+
+    for (int ti = blockIdx.x; ti < a.ntasks; ti += gridDim.x) {
+        const Task t = a.tasks[ti];
+        wait_turn(a, t);
+        const int nk = (t.k + kBK - 1) / kBK;
+#pragma unroll
+        for (int s = 0; s < STAGES - 1; ++s) {
+            if (s < nk) load_slab<BM, BN, NT, false, true>(smem + s * G::STAGE, smem + s * G::STAGE + G::A_ELEMS, a, t,
+                                                          t.p0 + s * kBK);
+            cp_commit();
+        }
+        const Dest d = resolve(a, t);
+        double acc[TM][TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                const int r = r0 + i, c = c0 + j;
+                acc[i][j] = (d.src && r < t.m && c < t.n)
+                                ? __ldcg(d.src + (t.i0 + r) + static_cast<int64_t>(t.j0 + c) * d.ld_src)
+                                : 0.0;
+            }
+
+        auto step = [&](const double* As, const double* Bt, int kk) {
+            double av[TM], bv[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) av[i] = As[kk * G::LDA + r0 + i];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) bv[j] = Bt[kk * G::LDB + c0 + j];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) {
+                    if constexpr (EXACT)
+                        acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(av[i], bv[j]));
+                    else
+                        acc[i][j] = __fma_rn(av[i], bv[j], acc[i][j]);
+                }
+        };
+
+        for (int s = 0; s < nk; ++s) {
+            cp_wait<STAGES - 2>();
+            __syncthreads();
+            const int nx = s + STAGES - 1;
+            if (nx < nk) {
+                double* st = smem + (nx % STAGES) * G::STAGE;
+                load_slab<BM, BN, NT, false, true>(st, st + G::A_ELEMS, a, t, t.p0 + nx * kBK);
+            }
+            cp_commit();
+            const double* As = smem + (s % STAGES) * G::STAGE;
+            const double* Bt = As + G::A_ELEMS;
+            const int kv = min(kBK, t.k - s * kBK);
+            if (kv == kBK) {
+#pragma unroll
+                for (int kk = 0; kk < kBK; ++kk) step(As, Bt, kk);
+            } else {
+                for (int kk = 0; kk < kv; ++kk) step(As, Bt, kk);
+            }
+        }
+        cp_wait<0>();
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                const int r = r0 + i, c = c0 + j;
+                if (r < t.m && c < t.n)
+                    d.dst[(static_cast<int64_t>(t.i0) + r) + (static_cast<int64_t>(t.j0) + c) * d.ld_dst] = acc[i][j];
+            }
+        signal_done(a, t);
+    }
+}
+
+// Deterministic split-k reduction: C = W[0] + W[1] + ... in slice order.
+__global__ void k_reduce(double* C, int64_t ldc, const double* W, int64_t wld, int64_t wslice, int slices, int64_t m,
+                         int64_t n) {
+    const int64_t total = m * n;
+    for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < total;
+         x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = x % m, j = x / m;
+        double s = W[i + j * wld];
+        for (int q = 1; q < slices; ++q) s = __dadd_rn(s, W[q * wslice + i + j * wld]);
+        C[i + j * ldc] = s;
+    }
+}
+
+// Counter-based uniform[-1,1): splitmix64 of (seed, index), top 53 bits.
+__global__ void k_fill(double* x, int64_t count, uint64_t seed, uint64_t offset) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + (offset + static_cast<uint64_t>(i) + 1) * 0x9E3779B97F4A7C15ULL;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        z ^= z >> 31;
+        const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
+        x[i] = 2.0 * u - 1.0;
+    }
+}
+
+// ------------------------------ registry ---------------------------------
+constexpr int kStagesBig = 4, kStagesSmall = 4, kStagesSimt = 3;
+
+template <int BM, int BN, bool BT, int STAGES>
+constexpr int smem_of() {
+    return Geo<BM, BN, BT>::STAGE * STAGES * static_cast<int>(sizeof(double));
+}
+
+struct Entry {
+    const void* fn[2];  // [vec16]
+    int tile_m, tile_n, threads, smem;
+};
+
+const Entry kTable[kKernelCount] = {
+    {{(const void*)k_dmma<128, 128, 64, 32, kStagesBig, false>, (const void*)k_dmma<128, 128, 64, 32, kStagesBig, true>},
+     128, 128, 256, smem_of<128, 128, false, kStagesBig>()},
+    {{(const void*)k_dmma<64, 64, 32, 32, kStagesSmall, false>, (const void*)k_dmma<64, 64, 32, 32, kStagesSmall, true>},
+     64, 64, 128, smem_of<64, 64, false, kStagesSmall>()},
+    {{(const void*)k_simt<64, 64, 4, 4, kStagesSimt, false>, (const void*)k_simt<64, 64, 4, 4, kStagesSimt, false>},
+     64, 64, 256, smem_of<64, 64, true, kStagesSimt>()},
+    {{(const void*)k_simt<64, 64, 4, 4, kStagesSimt, true>, (const void*)k_simt<64, 64, 4, 4, kStagesSimt, true>},
+     64, 64, 256, smem_of<64, 64, true, kStagesSimt>()},
+    {{(const void*)k_simt<128, 128, 8, 8, kStagesSimt, false>, (const void*)k_simt<128, 128, 8, 8, kStagesSimt, false>},
+     128, 128, 256, smem_of<128, 128, true, kStagesSimt>()},
+};
+
+KernelInfo g_info[kKernelCount];
+bool g_ready[kKernelCount][2];
+int g_device = -1;
+
+cudaError_t prepare(Kernel k, bool v16) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev != g_device) {
+        for (auto& r : g_ready) r[0] = r[1] = false;
+        g_device = dev;
+    }
+    if (g_ready[k][v16]) return cudaSuccess;
+    const Entry& en = kTable[k];
+    e = cudaFuncSetAttribute(en.fn[v16], cudaFuncAttributeMaxDynamicSharedMemorySize, en.smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, en.fn[v16], en.threads, en.smem);
+    if (e != cudaSuccess) return e;
+    g_info[k] = KernelInfo{en.tile_m, en.tile_n, en.threads, en.smem, occ};
+    g_ready[k][v16] = true;
+    return cudaSuccess;
+}
+
+}  // namespace
+
+cudaError_t kernel_info(Kernel kernel, KernelInfo* info) {
+    cudaError_t e = prepare(kernel, false);
+    if (e == cudaSuccess) *info = g_info[kernel];
+    return e;
+}
+
+cudaError_t launch(Kernel kernel, bool vec16, const Args& args, int grid, cudaStream_t stream) {
+    cudaError_t e = prepare(kernel, vec16);
+    if (e != cudaSuccess) return e;
+    if (args.ntasks <= 0) return cudaSuccess;
+    const Entry& en = kTable[kernel];
+    Args local = args;
+    void* params[] = {&local};
+    return cudaLaunchKernel(en.fn[vec16], dim3(grid), dim3(en.threads), params, en.smem, stream);
+}
+
+cudaError_t launch_reduce(double* C, int64_t ldc, const double* work, int64_t work_ld, int64_t work_slice, int slices,
+                          int64_t m, int64_t n, cudaStream_t stream) {
+    const int64_t total = m * n;
+    int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+    k_reduce<<<blocks, 256, 0, stream>>>(C, ldc, work, work_ld, work_slice, slices, m, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill(double* x, int64_t count, uint64_t seed, uint64_t offset, cudaStream_t stream) {
+    if (count <= 0) return cudaSuccess;
+    int blocks = static_cast<int>(std::min<int64_t>((count + 255) / 256, 148 * 32));
+    k_fill<<<blocks, 256, 0, stream>>>(x, count, seed, offset);
+    return cudaGetLastError();
+}
+
+}  // namespace gpu
+}  // namespace mmm

@@ -1,0 +1,66 @@
+// Interface between the host lowering (capi.cpp) and the sm_100a kernels
+// (dgemm_sm100.cu). A launch is a list of CTA tasks processed by a
+// persistent grid in list order (task t runs on CTA t mod grid).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace mmm {
+namespace gpu {
+
+// One CTA task: C(i0:i0+m, j0:j0+n) += A(i0:, p0:p0+k) · B(p0:, j0:j0+n),
+// accumulated in ascending k from the incoming C value (the reference's cell,
+// exec.hpp:35-46, at CTA granularity).
+struct Task {
+    int32_t i0, j0, p0;
+    int32_t m, n, k;
+    int32_t tile;   // progress counter of this C region (-1: no ordering needed)
+    int32_t seq;    // chunks of this region that must finish first
+    int32_t slice;  // -1: read/write C; s >= 0: split-k partial into workspace slice s
+    int32_t from_c; // slice tasks: 1 = start from C's value, 0 = start from zero
+};
+
+struct Args {
+    const double* A;
+    int64_t lda;
+    const double* B;
+    int64_t ldb;
+    double* C;
+    int64_t ldc;
+    const Task* tasks;
+    int32_t ntasks;
+    int32_t* progress;   // one counter per ordered region (faithful schedule)
+    double* work;        // split-k slices, column-major m x n each, ld = work_ld
+    int64_t work_ld;
+    int64_t work_slice;  // elements per slice
+};
+
+enum Kernel : int {
+    kDmma128 = 0,   // 128x128 C tile, 8 warps of 64x32, mma.sync m8n8k4 f64
+    kDmma64 = 1,    // 64x64 C tile, 4 warps of 32x32
+    kFma64 = 2,     // 64x64, DFMA chain per entry (bit-exact vs sequential fma)
+    kExact64 = 3,   // 64x64, DMUL + DADD per step (bit-exact vs the reference)
+    kFma128 = 4,    // 128x128, 8x8 per thread DFMA chain
+    kKernelCount = 5
+};
+
+struct KernelInfo {
+    int tile_m, tile_n, threads;
+    int smem_bytes;
+    int ctas_per_sm;  // occupancy measured at first use
+};
+
+// Launch `kernel` over args.tasks with `grid` persistent CTAs. vec16 selects
+// 16-byte cp.async staging (all task origins even, ld even, 16B-aligned bases).
+cudaError_t launch(Kernel kernel, bool vec16, const Args& args, int grid, cudaStream_t stream);
+// Occupancy-derived info (queries the device on first call).
+cudaError_t kernel_info(Kernel kernel, KernelInfo* info);
+// C = sum over slices in slice order (deterministic split-k reduction).
+cudaError_t launch_reduce(double* C, int64_t ldc, const double* work, int64_t work_ld, int64_t work_slice,
+                          int slices, int64_t m, int64_t n, cudaStream_t stream);
+cudaError_t launch_fill(double* x, int64_t count, uint64_t seed, uint64_t offset, cudaStream_t stream);
+
+}  // namespace gpu
+}  // namespace mmm

@@ -1,0 +1,593 @@
+"""The reference's `tilemul` interface for the execution path, backed by the
+B200-native library (C ABI in include/tilemul_b200.h).
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/tilemul/*.hpp so a caller of the reference (and
+the restated reference tests in tests/) reads the same:
+
+    d = parse_name("C2A1C0")
+    bs = derive_blocksizes(d, hier, Shape(2048, 2048, 2048))
+    nest = build_plan(d, bs, hier, shape)
+    execute(nest, A, B, C)            # C += A·B on the GPU
+
+Operands are column-major FP64: CUDA torch tensors (device path, async on
+the current stream) or numpy arrays (host path: copy in, run, copy back).
+Errors: ParseError (with .rule), ValidationFailure (with .violations),
+InfeasibleError, ValueError (the reference's std::invalid_argument),
+CudaError (device runtime failures).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Dict, Iterable, List, Optional, Sequence, Tuple
+
+from . import _native as N
+
+DIMS = ("m", "n", "k")
+OPERANDS = ("A", "B", "C")
+
+
+# ------------------------------------------------------------------ errors
+@dataclass(frozen=True)
+class Violation:  # types.hpp:132-138
+    rule: str
+    level: int = -1
+    lhs: int = 0
+    rhs: int = 0
+
+
+class ParseError(ValueError):  # types.hpp:148-154
+    def __init__(self, rule: str, msg: str):
+        super().__init__(msg)
+        self.rule = rule
+
+
+class ValidationFailure(RuntimeError):  # types.hpp:157-170
+    def __init__(self, violations: List[Violation], msg: str):
+        super().__init__(msg)
+        self.violations = violations
+
+
+class InfeasibleError(RuntimeError):  # types.hpp:173-176
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _rules() -> List[Violation]:
+    out = []
+    for ln in N.lib().tm_last_rules().decode().splitlines():
+        if not ln:
+            continue
+        r, lvl, lhs, rhs = ln.rsplit(":", 3)
+        out.append(Violation(r, int(lvl), int(lhs), int(rhs)))
+    return out
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = N.lib().tm_last_error().decode()
+    if rc == 1:
+        rules = _rules()
+        if msg.startswith("validation failed"):
+            raise ValidationFailure(rules, msg)
+        if rules and rules[0].rule == "infeasible":
+            raise InfeasibleError(msg)
+        raise ParseError(rules[0].rule if rules else "", msg)
+    if rc == 3:
+        raise CudaError(msg)
+    raise ValueError(msg)
+
+
+# -------------------------------------------------------------- vocabulary
+@dataclass(frozen=True)
+class Shape:  # types.hpp:103-129
+    m: int = 1
+    n: int = 1
+    k: int = 1
+
+    def __post_init__(self):
+        if self.m < 1 or self.n < 1 or self.k < 1:
+            raise ValueError("shape extents must be >= 1")
+
+    def extent(self, d: str) -> int:
+        return {"m": self.m, "n": self.n, "k": self.k}[d]
+
+    def flops(self) -> int:
+        return 2 * self.m * self.n * self.k
+
+    def rows(self, op: str) -> int:
+        return {"A": self.m, "B": self.k, "C": self.m}[op]
+
+    def cols(self, op: str) -> int:
+        return {"A": self.k, "B": self.n, "C": self.n}[op]
+
+
+@dataclass(frozen=True)
+class CacheLevel:  # cache.hpp:12-19
+    index: int
+    capacity_elements: int
+    granularity: int = 1
+    inclusive: bool = False
+    write_allocate: bool = True
+    write_back: bool = True
+
+
+class CacheHierarchy:  # cache.hpp:23-49
+    def __init__(self, levels: Sequence[CacheLevel]):
+        levels = list(levels)
+        if not levels:
+            raise ValueError("hierarchy needs at least one level")
+        for i, lv in enumerate(levels):
+            if lv.index != i:
+                raise ValueError("hierarchy level indices must be contiguous from 0")
+            if lv.capacity_elements < 1:
+                raise ValueError("cache capacity must be >= 1")
+            if lv.granularity < 1:
+                raise ValueError("cache granularity must be >= 1")
+            if i > 0 and lv.capacity_elements <= levels[i - 1].capacity_elements:
+                raise ValueError("cache capacities must strictly increase with level")
+        self._levels = levels
+
+    @classmethod
+    def from_capacities(cls, caps: Sequence[int], inclusive: Sequence[bool] = ()):
+        inc = list(inclusive) + [False] * (len(caps) - len(inclusive))
+        return cls([CacheLevel(i, int(c), 1, bool(inc[i])) for i, c in enumerate(caps)])
+
+    def size(self) -> int:
+        return len(self._levels)
+
+    def level(self, h: int) -> CacheLevel:
+        return self._levels[h]
+
+    def levels(self) -> List[CacheLevel]:
+        return list(self._levels)
+
+    def top_level(self) -> int:
+        return len(self._levels) - 1
+
+    def capacity(self, h: int) -> int:
+        return self._levels[h].capacity_elements
+
+    def _c(self):
+        arr = (N.tm_level * len(self._levels))()
+        for i, lv in enumerate(self._levels):
+            arr[i] = N.tm_level(lv.capacity_elements, lv.granularity, int(lv.inclusive), int(lv.write_allocate),
+                                int(lv.write_back))
+        return arr, len(self._levels)
+
+
+def gpu_hierarchy(tile: int = 128) -> CacheHierarchy:
+    """The current B200's hierarchy in FP64 elements: 0 = CTA C tile,
+    1 = shared memory per block, 2 = L2 (queried from the device)."""
+    arr = (N.tm_level * 8)()
+    cnt = C.c_int(0)
+    _check(N.lib().tm_gpu_hierarchy(tile, arr, 8, C.byref(cnt)))
+    return CacheHierarchy([CacheLevel(i, arr[i].capacity_elements) for i in range(cnt.value)])
+
+
+# ------------------------------------------------------------- descriptors
+@dataclass(frozen=True)
+class LevelPlan:  # descriptor.hpp:18-25
+    level: int
+    resident: str
+    outer_dim: str
+    inner_dim: str
+
+
+@dataclass
+class AlgorithmDescriptor:  # descriptor.hpp:30-43
+    plans: List[LevelPlan] = field(default_factory=list)
+    allow_non_c_registers: bool = False
+
+    def plan_at(self, level: int) -> Optional[LevelPlan]:
+        for p in self.plans:
+            if p.level == level:
+                return p
+        return None
+
+    def top_level(self) -> int:
+        return self.plans[0].level if self.plans else -1
+
+    def __eq__(self, other):
+        return isinstance(other, AlgorithmDescriptor) and self.plans == other.plans
+
+    @property
+    def name(self) -> str:
+        return format_name(self)
+
+
+def guest_operand(below: LevelPlan) -> str:  # descriptor.hpp:47
+    return {"n": "A", "m": "B", "k": "C"}[below.inner_dim]
+
+
+def _tiers_to_desc(arr, n, allow) -> AlgorithmDescriptor:
+    return AlgorithmDescriptor([LevelPlan(arr[i].level, arr[i].resident.decode(), arr[i].outer_dim.decode(),
+                                          arr[i].inner_dim.decode()) for i in range(n)], allow)
+
+
+def parse_name(text: str, allow_non_c_registers: bool = False) -> AlgorithmDescriptor:
+    arr = (N.tm_tier * 16)()
+    cnt = C.c_int(0)
+    _check(N.lib().tm_parse_name(text.encode(), int(allow_non_c_registers), arr, 16, C.byref(cnt)))
+    return _tiers_to_desc(arr, cnt.value, allow_non_c_registers)
+
+
+def make_descriptor(residents: Sequence[Tuple[int, str]], allow_non_c_registers: bool = False) -> AlgorithmDescriptor:
+    lv = (C.c_int32 * max(1, len(residents)))(*[r[0] for r in residents])
+    ops = "".join(r[1] for r in residents).encode()
+    arr = (N.tm_tier * 16)()
+    cnt = C.c_int(0)
+    name = C.create_string_buffer(64)
+    _check(N.lib().tm_compose(lv, ops, len(residents), int(allow_non_c_registers), name, 64, arr, 16, C.byref(cnt)))
+    return _tiers_to_desc(arr, cnt.value, allow_non_c_registers)
+
+
+def format_name(d: AlgorithmDescriptor) -> str:  # descriptor.hpp:128-136
+    s = ""
+    for p in d.plans:
+        if p.level > 9:
+            raise ValueError("names only cover cache levels 0..9")
+        s += f"{p.resident}{p.level}"
+    return s
+
+
+def validate_structure(d: AlgorithmDescriptor) -> List[Violation]:
+    arr = (N.tm_tier * max(1, len(d.plans)))()
+    for i, p in enumerate(d.plans):
+        arr[i] = N.tm_tier(p.level, p.resident.encode(), p.outer_dim.encode(), p.inner_dim.encode())
+    rc = N.lib().tm_validate_structure(arr, len(d.plans), int(d.allow_non_c_registers))
+    if rc < 0:
+        _check(-rc)
+    return _rules() if rc > 0 else []
+
+
+def skip_level(d: AlgorithmDescriptor, h: int) -> AlgorithmDescriptor:
+    out = C.create_string_buffer(64)
+    _check(N.lib().tm_skip_level(format_name(d).encode(), h, out, 64))
+    return parse_name(out.value.decode(), d.allow_non_c_registers)
+
+
+def select_algorithm(s: Shape, outer_capacity: int) -> str:
+    r = C.create_string_buffer(2)
+    _check(N.lib().tm_select_outer(s.m, s.n, s.k, outer_capacity, r))
+    return r.value.decode()
+
+
+# -------------------------------------------------------------- blocksizes
+class BlocksizeSet:  # blocksizes.hpp:22-56
+    def __init__(self, entries: Optional[Dict[Tuple[int, str], int]] = None):
+        self._v: Dict[Tuple[int, str], int] = {}
+        for (lv, d), v in (entries or {}).items():
+            self.set(lv, d, v)
+
+    def set(self, level: int, dim: str, value: int) -> None:
+        if value < 1:
+            raise ValueError("blocksize must be >= 1")
+        self._v[(int(level), dim)] = int(value)
+
+    def has(self, level: int, dim: str) -> bool:
+        return (level, dim) in self._v
+
+    def get(self, level: int, dim: str) -> int:
+        if (level, dim) not in self._v:
+            raise KeyError(f"no blocksize for level {level} dim {dim}")
+        return self._v[(level, dim)]
+
+    def entries(self) -> List[Tuple[Tuple[int, str], int]]:
+        return sorted(self._v.items(), key=lambda kv: (kv[0][0], DIMS.index(kv[0][1])))
+
+    def as_dict(self) -> Dict[Tuple[int, str], int]:
+        return dict(self._v)
+
+    def __eq__(self, other):
+        return isinstance(other, BlocksizeSet) and self._v == other._v
+
+    def __repr__(self):
+        return "BlocksizeSet(" + ", ".join(f"{lv}:{d}={v}" for (lv, d), v in self.entries()) + ")"
+
+    def _c(self):
+        ent = self.entries()
+        arr = (N.tm_blocksize * max(1, len(ent)))()
+        for i, ((lv, d), v) in enumerate(ent):
+            arr[i] = N.tm_blocksize(lv, d.encode(), v)
+        return arr, len(ent)
+
+
+@dataclass
+class AccessCosts:  # blocksizes.hpp:59-76
+    beta_a: float = 1.0
+    beta_b: float = 1.0
+    beta_c: float = 1.0
+
+
+@dataclass
+class MicroTile:  # blocksizes.hpp:79-82
+    m_r: int = 4
+    n_r: int = 12
+
+
+@dataclass
+class DeriveOptions:  # blocksizes.hpp:84-87
+    slack: float = 1.0 / 16.0
+    micro: MicroTile = field(default_factory=MicroTile)
+
+
+def derive_blocksizes(d: AlgorithmDescriptor, hier: CacheHierarchy, shape: Shape, costs: AccessCosts = None,
+                      opts: DeriveOptions = None, pinned: BlocksizeSet = None) -> BlocksizeSet:
+    costs = costs or AccessCosts()
+    opts = opts or DeriveOptions()
+    pinned = pinned or BlocksizeSet()
+    h, nh = hier._c()
+    p, npin = pinned._c()
+    o = N.tm_derive_opts(opts.slack, opts.micro.m_r, opts.micro.n_r, costs.beta_a, costs.beta_b, costs.beta_c)
+    out = (N.tm_blocksize * 64)()
+    cnt = C.c_int(0)
+    _check(N.lib().tm_derive(format_name(d).encode(), h, nh, shape.m, shape.n, shape.k, C.byref(o), p, npin, out, 64,
+                             C.byref(cnt)))
+    return BlocksizeSet({(out[i].level, out[i].dim.decode()): out[i].value for i in range(cnt.value)})
+
+
+def validate_blocksizes(d: AlgorithmDescriptor, bs: BlocksizeSet, hier: CacheHierarchy, shape: Shape) -> List[Violation]:
+    h, nh = hier._c()
+    b, nb = bs._c()
+    rc = N.lib().tm_validate(format_name(d).encode(), h, nh, shape.m, shape.n, shape.k, b, nb)
+    if rc < 0:
+        _check(-rc)
+    return _rules() if rc > 0 else []
+
+
+@dataclass(frozen=True)
+class NestStep:  # blocksizes.hpp:428-434
+    level: int
+    dim: str
+    blocksize: int
+    cap: bool = False
+
+
+# ------------------------------------------------------------------- model
+@dataclass
+class OperandTraffic:
+    reads: int = 0
+    writes: int = 0
+
+    def total(self) -> int:
+        return self.reads + self.writes
+
+
+@dataclass
+class LevelTraffic:
+    level: int
+    per_operand: Dict[str, OperandTraffic]
+
+    def of(self, op: str) -> OperandTraffic:
+        return self.per_operand[op]
+
+    def reads(self) -> int:
+        return sum(t.reads for t in self.per_operand.values())
+
+    def writes(self) -> int:
+        return sum(t.writes for t in self.per_operand.values())
+
+    def total_elements(self) -> int:
+        return self.reads() + self.writes()
+
+    def total_bytes(self, elem_bytes: Dict[str, float] = None) -> float:
+        eb = elem_bytes or {"A": 8, "B": 8, "C": 8}
+        return sum(eb[o] * (t.reads + t.writes) for o, t in self.per_operand.items())
+
+
+@dataclass
+class CostReport:  # costmodel.hpp:44-62
+    shape: Shape
+    flops: int
+    levels: List[LevelTraffic]
+    boundary_level: int
+
+    def at_level(self, h: int) -> LevelTraffic:
+        for lt in self.levels:
+            if lt.level == h:
+                return lt
+        raise KeyError(f"no traffic entry for level {h}")
+
+    def intensity_flops_per_byte(self) -> float:
+        b = self.at_level(self.boundary_level).total_bytes()
+        return float("inf") if b == 0 else self.flops / b
+
+
+def _report(shape: Shape, raw, nlev: int) -> CostReport:
+    levels = []
+    for h in range(nlev):
+        levels.append(LevelTraffic(h, {op: OperandTraffic(raw[(h * 3 + i) * 2], raw[(h * 3 + i) * 2 + 1])
+                                       for i, op in enumerate(OPERANDS)}))
+    return CostReport(shape, shape.flops(), levels, nlev - 1)
+
+
+def multilevel_cost(d: AlgorithmDescriptor, bs: BlocksizeSet, hier: CacheHierarchy, shape: Shape,
+                    boundary_level: int = -1) -> CostReport:
+    h, nh = hier._c()
+    b, nb = bs._c()
+    raw = (C.c_int64 * (nh * 6))()
+    _check(N.lib().tm_model(format_name(d).encode(), int(d.allow_non_c_registers), h, nh, shape.m, shape.n, shape.k,
+                            b, nb, raw, nh * 6))
+    rep = _report(shape, raw, nh)
+    if boundary_level >= 0:
+        rep.boundary_level = boundary_level
+    return rep
+
+
+def io_lower_bound(s: Shape, M: int) -> OperandTraffic:
+    r, w = C.c_int64(0), C.c_int64(0)
+    _check(N.lib().tm_io_lower_bound(s.m, s.n, s.k, M, C.byref(r), C.byref(w)))
+    return OperandTraffic(r.value, w.value)
+
+
+def resident_cost(variant: str, s: Shape, b_first: int, b_second: int) -> LevelTraffic:
+    raw = (C.c_int64 * 6)()
+    _check(N.lib().tm_resident_cost(variant.encode(), s.m, s.n, s.k, b_first, b_second, raw))
+    return LevelTraffic(0, {op: OperandTraffic(raw[i * 2], raw[i * 2 + 1]) for i, op in enumerate(OPERANDS)})
+
+
+def _dbl(v: float) -> float:
+    if v < 0:
+        raise ValueError(N.lib().tm_last_error().decode())
+    return v
+
+
+def streaming_efficiency(variant: str, b_first: int, b_second: int) -> float:
+    return _dbl(N.lib().tm_streaming_efficiency(variant.encode(), b_first, b_second))
+
+
+def goto_efficiency(k_c: int, n_c: int) -> float:
+    return _dbl(N.lib().tm_goto_efficiency(k_c, n_c))
+
+
+def efficiency(report: CostReport, level: int = -1, write_weight: float = 1.0) -> Tuple[float, float]:
+    lt = report.at_level(report.boundary_level if level < 0 else level)
+    el = lt.reads() + write_weight * lt.writes()
+    if el <= 0:
+        return float("inf"), float("inf")
+    fpe = report.flops / el
+    return fpe, fpe / 8.0
+
+
+def roofline_bound(intensity: float, peak: float, bandwidth: float) -> float:
+    return _dbl(N.lib().tm_roofline_bound(intensity, peak, bandwidth))
+
+
+# --------------------------------------------------------------- the plan
+NUMERICS = {"dmma": 0, "fma": 1, "exact": 2}
+SCHEDULES = {"fused": 0, "faithful": 1}
+
+
+@dataclass
+class ExecOptions:  # exec.hpp:48-53, re-targeted
+    numerics: str = "dmma"      # dmma | fma | exact
+    schedule: str = "fused"     # fused | faithful
+    split_k: int = 1            # fused: k slices with a fixed-order reduction (0 = auto)
+    ctas: int = 0               # persistent grid (0 = SMs x occupancy)
+    tile: int = 0               # CTA tile edge 64/128 (0 = from the register tile)
+
+    def _c(self):
+        return N.tm_exec_opts(NUMERICS[self.numerics], SCHEDULES[self.schedule], self.split_k, self.ctas, self.tile)
+
+
+class LoopNest:  # plan.hpp:25-85
+    """An executable nest on the GPU. Owns the native plan."""
+
+    def __init__(self, d: AlgorithmDescriptor, bs: BlocksizeSet, hier: CacheHierarchy, shape: Shape):
+        h, nh = hier._c()
+        b, nb = bs._c()
+        ptr = C.c_void_p(None)
+        _check(N.lib().tm_plan_create(format_name(d).encode(), h, nh, shape.m, shape.n, shape.k, b, nb,
+                                      C.byref(ptr)))
+        self._ptr = ptr
+        self.shape = shape
+        self.descriptor = d
+        self.blocksizes = bs
+        self.hierarchy = hier
+        arr = (N.tm_loop * 64)()
+        cnt = C.c_int(0)
+        _check(N.lib().tm_plan_loops(self._ptr, arr, 64, C.byref(cnt)))
+        self.loops = [NestStep(arr[i].level, arr[i].dim.decode(), arr[i].blocksize, bool(arr[i].cap))
+                      for i in range(cnt.value)]
+        self.m_r = bs.get(0, "m")
+        self.n_r = bs.get(0, "n")
+
+    def __del__(self):
+        p = getattr(self, "_ptr", None)
+        if p is not None and p.value:
+            N.lib().tm_plan_destroy(p)
+            self._ptr = None
+
+    def cell_count(self) -> int:
+        return int(N.lib().tm_plan_cells(self._ptr))
+
+    def model(self) -> CostReport:
+        nh = N.lib().tm_plan_levels(self._ptr)
+        raw = (C.c_int64 * (nh * 6))()
+        _check(N.lib().tm_plan_model(self._ptr, raw, nh * 6))
+        return _report(self.shape, raw, nh)
+
+    def last_launch(self) -> Dict[str, int]:
+        t, l, c = C.c_int64(0), C.c_int32(0), C.c_int32(0)
+        _check(N.lib().tm_plan_last_launch(self._ptr, C.byref(t), C.byref(l), C.byref(c)))
+        return {"tasks": t.value, "launches": l.value, "ctas": c.value}
+
+
+def build_plan(d: AlgorithmDescriptor, bs: BlocksizeSet, hier: CacheHierarchy, shape: Shape) -> LoopNest:
+    return LoopNest(d, bs, hier, shape)
+
+
+# --------------------------------------------------------------- execute
+def _colmajor_view(x, rows: int, cols: int, name: str):
+    """(pointer, leading dim, is_device) of a column-major FP64 operand."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(x, torch.Tensor):
+        if x.dtype != torch.float64:
+            raise ValueError(f"{name} must be float64")
+        if x.dim() == 1:
+            if x.numel() != rows * cols or x.stride(0) != 1:
+                raise ValueError(f"{name} extents do not match the plan's shape")
+            ld = rows
+        elif x.dim() == 2:
+            if tuple(x.shape) != (rows, cols) or x.stride(0) != 1:
+                raise ValueError(f"{name} must be a column-major {rows}x{cols} view (stride(0) == 1)")
+            ld = max(x.stride(1), rows)
+        else:
+            raise ValueError(f"{name} must be 1-D or 2-D")
+        return x.data_ptr(), ld, x.is_cuda
+    import numpy as np
+
+    if not isinstance(x, np.ndarray) or x.dtype != np.float64:
+        raise ValueError(f"{name} must be a float64 numpy array or torch tensor")
+    if x.size != rows * cols:
+        raise ValueError(f"{name} extents do not match the plan's shape")
+    if x.ndim == 2 and not (x.shape == (rows, cols) and x.flags.f_contiguous):
+        raise ValueError(f"{name} must be a Fortran-ordered {rows}x{cols} array")
+    if x.ndim == 1 and not x.flags.c_contiguous:
+        raise ValueError(f"{name} must be contiguous")
+    return x.ctypes.data, rows, False
+
+
+def execute(nest: LoopNest, A, B, C_, opts: ExecOptions = None, stream=None) -> None:
+    """C += A·B through the nest on the GPU (exec.hpp:94-138).
+
+    Device tensors: asynchronous on `stream` (a torch.cuda.Stream, a raw
+    cudaStream_t int, or None = torch's current stream). Host numpy arrays:
+    synchronous copy-in / run / copy-out."""
+    opts = opts or ExecOptions()
+    s = nest.shape
+    pa, lda, da = _colmajor_view(A, s.m, s.k, "A")
+    pb, ldb, db = _colmajor_view(B, s.k, s.n, "B")
+    pc, ldc, dc = _colmajor_view(C_, s.m, s.n, "C")
+    o = opts._c()
+    if da and db and dc:
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream().cuda_stream
+        elif hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        _check(N.lib().tm_execute(nest._ptr, pa, lda, pb, ldb, pc, ldc, C.byref(o), C.c_void_p(stream)))
+    elif not (da or db or dc):
+        if lda != s.m or ldb != s.k or ldc != s.m:
+            raise ValueError("host operands must be dense column-major")
+        _check(N.lib().tm_execute_host(nest._ptr, pa, pb, pc, C.byref(o)))
+    else:
+        raise ValueError("operands must be all on the device or all on the host")
+
+
+def fill_uniform_device(x, seed: int, offset: int = 0, stream=None) -> None:
+    """Counter-based uniform[-1,1) fill of a CUDA float64 tensor."""
+    import torch
+
+    st = torch.cuda.current_stream().cuda_stream if stream is None else getattr(stream, "cuda_stream", stream)
+    _check(N.lib().tm_fill_uniform_device(x.data_ptr(), x.numel(), seed, offset, C.c_void_p(st)))
