@@ -159,6 +159,10 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
 /* Number of CTA tasks and kernel launches the last tm_execute issued. */
 int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, int32_t* ctas);
 
+/* Sustained FP64 tensor-pipe (DMMA) rate of the current device in TFLOP/s,
+ * from `launches` ~7 ms probe launches: the roofline denominator. */
+int tm_measure_fp64_peak(int launches, double* tflops);
+
 /* --- seeded device inputs ------------------------------------------------ */
 /* Counter-based uniform[-1,1) generator on the device (for operands too large
  * to produce on the host): v = 2u - 1 with u from splitmix64(seed, index). */

@@ -551,6 +551,10 @@ int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, 
     });
 }
 
+int tm_measure_fp64_peak(int launches, double* tflops) {
+    return guard([&] { cuda_check(gpu::measure_fp64_peak(launches < 1 ? 1 : launches, tflops), "fp64 peak probe"); });
+}
+
 int tm_fill_uniform_device(double* x, int64_t count, uint64_t seed, uint64_t offset, void* stream) {
     return guard([&] {
         cuda_check(gpu::launch_fill(x, count, seed, offset, static_cast<cudaStream_t>(stream)), "fill launch");

@@ -156,12 +156,105 @@ __device__ __forceinline__ void load_slab(double* As, double* Bs, const Args& a,
     }
 }
 
+
+// Element-granular staging (any alignment, any origin) for the DMMA kernel's
+// non-16B path: As[k][m] (stride BM+4), Bs[n][k] (stride BK+4).
+template <int BM, int BN, int BK, int NT>
+__device__ __forceinline__ void load_slab_generic(double* As, double* Bs, const Args& a, const Task& t, int p) {
+    constexpr int LDA = BM + 4, LDB = BK + 4;
+    const int tid = threadIdx.x;
+    const int klim = t.p0 + t.k - p;
+    const double* Ab = a.A + static_cast<int64_t>(t.i0) + static_cast<int64_t>(p) * a.lda;
+    const double* Bb = a.B + static_cast<int64_t>(p) + static_cast<int64_t>(t.j0) * a.ldb;
+#pragma unroll 4
+    for (int q = tid; q < BM * BK; q += NT) {
+        const int c = q / BM, r = q % BM;
+        const bool v = c < klim && r < t.m;
+        cp8(As + c * LDA + r, v ? Ab + r + static_cast<int64_t>(c) * a.lda : a.A, v ? 8 : 0);
+    }
+#pragma unroll 4
+    for (int q = tid; q < BN * BK; q += NT) {
+        const int n = q / BK, c = q % BK;
+        const bool v = c < klim && n < t.n;
+        cp8(Bs + n * LDB + c, v ? Bb + c + static_cast<int64_t>(n) * a.ldb : a.B, v ? 8 : 0);
+    }
+}
+
 // ============================== DMMA kernel ==============================
-template <int BM, int BN, int WM, int WN, int STAGES, bool V16>
+// Per-task staging state for the 16-byte path: every thread owns a fixed set
+// of 16B chunks of the A and B slabs, so source pointers, shared-memory
+// offsets and row/column validity are computed once per task; per slab only
+// the k validity (last slab) changes. The chunks are issued between the DMMA
+// groups of the current slab so the staging instructions fill issue slots
+// the FP64 pipe leaves idle.
+template <int BM, int BN, int BK, int NT>
+struct Stager {
+    static constexpr int LDA = BM + 4, LDB = BK + 4;
+    static constexpr int A_ELEMS = BK * LDA, STAGE = A_ELEMS + BN * LDB;
+    static constexpr int A_PER_COL = BM / 2, B_PER_COL = BK / 2;
+    static constexpr int A_CH = BM * BK / 2 / NT, B_CH = BN * BK / 2 / NT;
+    static constexpr int A_CSTEP = NT / A_PER_COL, B_NSTEP = NT / B_PER_COL;
+    static_assert(NT % A_PER_COL == 0 && NT % B_PER_COL == 0, "thread count must tile the slab");
+    const double* a;  // A(i0 + ar, p0 + ac0)
+    const double* b;  // B(p0 + bc, j0 + bn0)
+    int64_t a_ld, b_ld;
+    int ac0, bc;      // k offsets of this thread's chunks within a slab
+    int a_bytes;      // 16/8/0: rows ar, ar+1 inside the task
+    uint32_t b_nvalid;  // bit it: column bn0 + it*B_NSTEP inside the task
+    uint32_t a_dst, b_dst;  // shared byte addresses in stage 0
+    const double* a_any;
+    const double* b_any;
+
+    __device__ __forceinline__ void init(const Args& g, const Task& t, const double* smem) {
+        const int tid = threadIdx.x;
+        const int ar = (tid % A_PER_COL) * 2;
+        ac0 = tid / A_PER_COL;
+        bc = (tid % B_PER_COL) * 2;
+        const int bn0 = tid / B_PER_COL;
+        a_ld = g.lda;
+        b_ld = g.ldb;
+        a = g.A + static_cast<int64_t>(t.i0) + ar + static_cast<int64_t>(t.p0 + ac0) * g.lda;
+        b = g.B + static_cast<int64_t>(t.p0) + bc + static_cast<int64_t>(t.j0 + bn0) * g.ldb;
+        a_bytes = min(max(t.m - ar, 0), 2) * 8;
+        b_nvalid = 0;
+#pragma unroll
+        for (int it = 0; it < B_CH; ++it) b_nvalid |= (bn0 + it * B_NSTEP < t.n ? 1u : 0u) << it;
+        a_dst = smem_addr(smem + ac0 * LDA + ar);
+        b_dst = smem_addr(smem + A_ELEMS + bn0 * LDB + bc);
+        a_any = g.A;
+        b_any = g.B;
+    }
+    // klim = valid k columns from this slab's start (>= BK for interior slabs)
+    __device__ __forceinline__ void issue_a(int slab, int stage, int klim) const {
+        const double* src = a + static_cast<int64_t>(slab) * BK * a_ld;
+        const uint32_t dst = a_dst + stage * STAGE * 8;
+#pragma unroll
+        for (int it = 0; it < A_CH; ++it) {
+            const int bytes = (ac0 + it * A_CSTEP < klim) ? a_bytes : 0;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + it * A_CSTEP * LDA * 8),
+                         "l"(bytes ? src + static_cast<int64_t>(it) * A_CSTEP * a_ld : a_any), "r"(bytes)
+                         : "memory");
+        }
+    }
+    __device__ __forceinline__ void issue_b(int slab, int stage, int klim) const {
+        const double* src = b + static_cast<int64_t>(slab) * BK;
+        const uint32_t dst = b_dst + stage * STAGE * 8;
+        const int kb = min(max(klim - bc, 0), 2) * 8;
+#pragma unroll
+        for (int it = 0; it < B_CH; ++it) {
+            const int bytes = ((b_nvalid >> it) & 1u) ? kb : 0;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + it * B_NSTEP * LDB * 8),
+                         "l"(bytes ? src + static_cast<int64_t>(it) * B_NSTEP * b_ld : b_any), "r"(bytes)
+                         : "memory");
+        }
+    }
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V16>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) {
     constexpr int NWM = BM / WM, NT = (BM / WM) * (BN / WN) * 32;
-    constexpr int FM = WM / 8, FN = WN / 8;
-    using G = Geo<BM, BN, false>;
+    constexpr int FM = WM / 8, FN = WN / 8, KK = BK / 4;
+    using S = Stager<BM, BN, BK, NT>;
     extern __shared__ __align__(128) double smem[];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -171,11 +264,20 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
     for (int ti = blockIdx.x; ti < a.ntasks; ti += gridDim.x) {
         const Task t = a.tasks[ti];
         wait_turn(a, t);
-        const int nk = (t.k + kBK - 1) / kBK;
+        const int nk = (t.k + BK - 1) / BK;
+        S st;
+        if constexpr (V16) st.init(a, t, smem);
 #pragma unroll
         for (int s = 0; s < STAGES - 1; ++s) {
-            if (s < nk) load_slab<BM, BN, NT, V16, false>(smem + s * G::STAGE, smem + s * G::STAGE + G::A_ELEMS, a, t,
-                                                         t.p0 + s * kBK);
+            if (s < nk) {
+                if constexpr (V16) {
+                    st.issue_a(s, s, t.k - s * BK);
+                    st.issue_b(s, s, t.k - s * BK);
+                } else {
+                    load_slab_generic<BM, BN, BK, NT>(smem + s * S::STAGE, smem + s * S::STAGE + S::A_ELEMS, a, t,
+                                                      t.p0 + s * BK);
+                }
+            }
             cp_commit();
         }
 
@@ -197,24 +299,33 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
             cp_wait<STAGES - 2>();
             __syncthreads();
             const int nx = s + STAGES - 1;
-            if (nx < nk) {
-                double* st = smem + (nx % STAGES) * G::STAGE;
-                load_slab<BM, BN, NT, V16, false>(st, st + G::A_ELEMS, a, t, t.p0 + nx * kBK);
-            }
-            cp_commit();
-            const double* As = smem + (s % STAGES) * G::STAGE;
-            const double* Bs = As + G::A_ELEMS;
+            const int nstage = nx % STAGES;
+            const double* As = smem + (s % STAGES) * S::STAGE;
+            const double* Bs = As + S::A_ELEMS;
 #pragma unroll
-            for (int kk = 0; kk < kBK / 4; ++kk) {
+            for (int kk = 0; kk < KK; ++kk) {
                 double af[FM], bf[FN];
 #pragma unroll
-                for (int mi = 0; mi < FM; ++mi) af[mi] = As[(kk * 4 + tq) * G::LDA + wm0 + mi * 8 + g];
+                for (int mi = 0; mi < FM; ++mi) af[mi] = As[(kk * 4 + tq) * S::LDA + wm0 + mi * 8 + g];
 #pragma unroll
-                for (int ni = 0; ni < FN; ++ni) bf[ni] = Bs[(wn0 + ni * 8 + g) * G::LDB + kk * 4 + tq];
+                for (int ni = 0; ni < FN; ++ni) bf[ni] = Bs[(wn0 + ni * 8 + g) * S::LDB + kk * 4 + tq];
 #pragma unroll
                 for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
                     for (int ni = 0; ni < FN; ++ni) dmma884(acc[mi][ni], af[mi], bf[ni]);
+                // stage the slab STAGES-1 ahead between the DMMA groups
+                if (kk == 0 && nx < nk) {
+                    if constexpr (V16) {
+                        st.issue_a(nx, nstage, t.k - nx * BK);
+                    } else {
+                        double* sp = smem + nstage * S::STAGE;
+                        load_slab_generic<BM, BN, BK, NT>(sp, sp + S::A_ELEMS, a, t, t.p0 + nx * BK);
+                    }
+                }
+                if (kk == (KK > 1 ? 1 : 0) && nx < nk) {
+                    if constexpr (V16) st.issue_b(nx, nstage, t.k - nx * BK);
+                }
+                if (kk == (KK > 1 ? 1 : 0)) cp_commit();
             }
         }
         cp_wait<0>();
@@ -345,7 +456,13 @@ __global__ void k_fill(double* x, int64_t count, uint64_t seed, uint64_t offset)
 }
 
 // ------------------------------ registry ---------------------------------
-constexpr int kStagesBig = 4, kStagesSmall = 4, kStagesSimt = 3;
+constexpr int kStagesBig = 3, kStagesSmall = 4, kStagesSimt = 3;
+constexpr int kBKBig = 32, kBKSmall = 16;
+
+template <int BM, int BN, int BK, int STAGES>
+constexpr int dmma_smem() {
+    return ((BM + 4) * BK + BN * (BK + 4)) * STAGES * static_cast<int>(sizeof(double));
+}
 
 template <int BM, int BN, bool BT, int STAGES>
 constexpr int smem_of() {
@@ -358,10 +475,10 @@ struct Entry {
 };
 
 const Entry kTable[kKernelCount] = {
-    {{(const void*)k_dmma<128, 128, 64, 32, kStagesBig, false>, (const void*)k_dmma<128, 128, 64, 32, kStagesBig, true>},
-     128, 128, 256, smem_of<128, 128, false, kStagesBig>()},
-    {{(const void*)k_dmma<64, 64, 32, 32, kStagesSmall, false>, (const void*)k_dmma<64, 64, 32, 32, kStagesSmall, true>},
-     64, 64, 128, smem_of<64, 64, false, kStagesSmall>()},
+    {{(const void*)k_dmma<128, 128, kBKBig, 64, 32, kStagesBig, false>, (const void*)k_dmma<128, 128, kBKBig, 64, 32, kStagesBig, true>},
+     128, 128, 256, dmma_smem<128, 128, kBKBig, kStagesBig>()},
+    {{(const void*)k_dmma<64, 64, kBKSmall, 32, 32, kStagesSmall, false>, (const void*)k_dmma<64, 64, kBKSmall, 32, 32, kStagesSmall, true>},
+     64, 64, 128, dmma_smem<64, 64, kBKSmall, kStagesSmall>()},
     {{(const void*)k_simt<64, 64, 4, 4, kStagesSimt, false>, (const void*)k_simt<64, 64, 4, 4, kStagesSimt, false>},
      64, 64, 256, smem_of<64, 64, true, kStagesSimt>()},
     {{(const void*)k_simt<64, 64, 4, 4, kStagesSimt, true>, (const void*)k_simt<64, 64, 4, 4, kStagesSimt, true>},

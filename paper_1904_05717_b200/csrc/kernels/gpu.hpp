@@ -60,6 +60,8 @@ cudaError_t kernel_info(Kernel kernel, KernelInfo* info);
 // C = sum over slices in slice order (deterministic split-k reduction).
 cudaError_t launch_reduce(double* C, int64_t ldc, const double* work, int64_t work_ld, int64_t work_slice,
                           int slices, int64_t m, int64_t n, cudaStream_t stream);
+// Sustained FP64 DMMA rate of this device (TFLOP/s) over `launches` probe launches.
+cudaError_t measure_fp64_peak(int launches, double* tflops);
 cudaError_t launch_fill(double* x, int64_t count, uint64_t seed, uint64_t offset, cudaStream_t stream);
 
 }  // namespace gpu

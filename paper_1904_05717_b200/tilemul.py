@@ -591,3 +591,10 @@ def fill_uniform_device(x, seed: int, offset: int = 0, stream=None) -> None:
 
     st = torch.cuda.current_stream().cuda_stream if stream is None else getattr(stream, "cuda_stream", stream)
     _check(N.lib().tm_fill_uniform_device(x.data_ptr(), x.numel(), seed, offset, C.c_void_p(st)))
+
+
+def measure_fp64_peak(launches: int = 20) -> float:
+    """Sustained FP64 DMMA TFLOP/s of the current device (roofline denominator)."""
+    v = C.c_double(0)
+    _check(N.lib().tm_measure_fp64_peak(launches, C.byref(v)))
+    return v.value
