@@ -167,6 +167,11 @@ int tm_measure_fp64_peak(int launches, double* tflops);
 /* Counter-based uniform[-1,1) generator on the device (for operands too large
  * to produce on the host): v = 2u - 1 with u from splitmix64(seed, index). */
 int tm_fill_uniform_device(double* x, int64_t count, uint64_t seed, uint64_t offset, void* stream);
+/* Block (row0.., col0..) of a global column-major matrix (leading dimension
+ * global_ld) filled with the same counter-based values, stored at x with
+ * leading dimension ld: every rank can generate its own block. */
+int tm_fill_uniform_block(double* x, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
+                          int64_t col0, int64_t global_ld, void* stream);
 
 #ifdef __cplusplus
 }

@@ -244,3 +244,16 @@ def ref_execute(name, caps, shape, bs, a, b, c, workers=1, parallel_loop=-1, pac
     if rc != 0:
         raise ValueError(f"rc={rc}: {err.value.decode()}")
     return secs.value
+
+
+def counter_uniform(seed: int, index):
+    """The device generator (tm_fill_uniform_*), restated in numpy:
+    v = 2u - 1, u = top 53 bits of splitmix64(seed + (index + 1) * golden)."""
+    idx = np.asarray(index, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + (idx + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    return 2.0 * u - 1.0

@@ -555,6 +555,16 @@ int tm_measure_fp64_peak(int launches, double* tflops) {
     return guard([&] { cuda_check(gpu::measure_fp64_peak(launches < 1 ? 1 : launches, tflops), "fp64 peak probe"); });
 }
 
+int tm_fill_uniform_block(double* x, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
+                          int64_t col0, int64_t global_ld, void* stream) {
+    return guard([&] {
+        if (ld < rows) fail_usage("leading dimension smaller than the block's row count");
+        cuda_check(gpu::launch_fill_block(x, rows, cols, ld, seed, row0, col0, global_ld,
+                                          static_cast<cudaStream_t>(stream)),
+                   "fill launch");
+    });
+}
+
 int tm_fill_uniform_device(double* x, int64_t count, uint64_t seed, uint64_t offset, void* stream) {
     return guard([&] {
         cuda_check(gpu::launch_fill(x, count, seed, offset, static_cast<cudaStream_t>(stream)), "fill launch");

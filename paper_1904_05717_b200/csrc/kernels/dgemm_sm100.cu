@@ -442,16 +442,33 @@ __global__ void k_reduce(double* C, int64_t ldc, const double* W, int64_t wld, i
     }
 }
 
-// Counter-based uniform[-1,1): splitmix64 of (seed, index), top 53 bits.
+// Counter-based uniform[-1,1): v = 2u - 1, u = top 53 bits of
+// splitmix64(seed + (index + 1) * golden). `index` is the element's position
+// in the GLOBAL column-major matrix, so any block of a distributed matrix is
+// reproducible from (seed, row, col) alone (oracle/oracle.py restates it).
+__device__ __forceinline__ double counter_uniform(uint64_t seed, uint64_t index) {
+    uint64_t z = seed + (index + 1) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return 2.0 * (static_cast<double>(z >> 11) * 0x1.0p-53) - 1.0;
+}
+
 __global__ void k_fill(double* x, int64_t count, uint64_t seed, uint64_t offset) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        uint64_t z = seed + (offset + static_cast<uint64_t>(i) + 1) * 0x9E3779B97F4A7C15ULL;
-        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-        z ^= z >> 31;
-        const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
-        x[i] = 2.0 * u - 1.0;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        x[i] = counter_uniform(seed, offset + static_cast<uint64_t>(i));
+}
+
+// x(i, j) (ld) = value of global element (row0 + i, col0 + j) of a matrix
+// with global leading dimension gld.
+__global__ void k_fill_block(double* x, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
+                             int64_t col0, int64_t gld) {
+    const int64_t total = rows * cols;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = q % rows, j = q / rows;
+        x[i + j * ld] = counter_uniform(seed, static_cast<uint64_t>((row0 + i) + (col0 + j) * gld));
     }
 }
 
@@ -534,6 +551,14 @@ cudaError_t launch_reduce(double* C, int64_t ldc, const double* work, int64_t wo
     const int64_t total = m * n;
     int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
     k_reduce<<<blocks, 256, 0, stream>>>(C, ldc, work, work_ld, work_slice, slices, m, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_block(double* x, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
+                              int64_t col0, int64_t gld, cudaStream_t stream) {
+    if (rows <= 0 || cols <= 0) return cudaSuccess;
+    int blocks = static_cast<int>(std::min<int64_t>((rows * cols + 255) / 256, 148 * 32));
+    k_fill_block<<<blocks, 256, 0, stream>>>(x, rows, cols, ld, seed, row0, col0, gld);
     return cudaGetLastError();
 }
 

@@ -62,6 +62,8 @@ cudaError_t launch_reduce(double* C, int64_t ldc, const double* work, int64_t wo
                           int slices, int64_t m, int64_t n, cudaStream_t stream);
 // Sustained FP64 DMMA rate of this device (TFLOP/s) over `launches` probe launches.
 cudaError_t measure_fp64_peak(int launches, double* tflops);
+cudaError_t launch_fill_block(double* x, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
+                              int64_t col0, int64_t gld, cudaStream_t stream);
 cudaError_t launch_fill(double* x, int64_t count, uint64_t seed, uint64_t offset, cudaStream_t stream);
 
 }  // namespace gpu

@@ -1,0 +1,224 @@
+"""Multi-GPU driver: C 2-D block-partitioned over a Pr x Pc process grid, A
+row-panels and B column-panels exchanged over NCCL in k-chunks, overlapped
+with the local blocked GEMM (BASELINE.json configs[4]).
+
+One process per GPU. Rank (r, c) owns
+  C_rc  — rows r*mL.., cols c*nL..            (mL x nL, column-major)
+  A_rc  — rows r*mL.., the k-chunks owned by c (mL x K/Pc, column-major)
+  B_rc  — the k-chunks owned by r, cols c*nL.. (stored chunk-major: each
+          KC x nL chunk contiguous column-major — the hierarchical
+          "prepacked" layout the reference uses for operands,
+          layout.hpp:17-98, so a chunk is one contiguous message)
+K is cut into L = lcm(Pr, Pc) * S chunks of KC; chunk j's A columns live on
+row-rank j // (L/Pc), its B rows on column-rank j // (L/Pr). Step j
+broadcasts A chunk j along the process row and B chunk j along the process
+column (NCCL, on NCCL's stream) while the local GEMM of chunk j-1 runs on
+the compute stream; k is never split across ranks, so there is no reduction
+and every C entry still accumulates in ascending k.
+
+The data movement is plain torch.distributed (NCCL on GPUs, gloo in the CPU
+tests); the local GEMM is `tilemul.execute` on the sm_100a task kernel. The
+`gemm` hook exists so the CPU tests can drive the same schedule with a
+host matmul — the product path always passes the native GEMM.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable, Optional, Tuple
+
+
+def grid_shape(P: int) -> Tuple[int, int]:
+    """Pr x Pc = P with Pr <= Pc and Pr as large as possible (1x1, 1x2, 2x2, 2x4)."""
+    pr = int(math.isqrt(P))
+    while P % pr:
+        pr -= 1
+    return pr, P // pr
+
+
+@dataclass(frozen=True)
+class Layout:
+    P: int
+    Pr: int
+    Pc: int
+    mL: int
+    nL: int
+    K: int
+    chunks: int   # L
+    KC: int
+
+    @property
+    def M(self) -> int:
+        return self.mL * self.Pr
+
+    @property
+    def N(self) -> int:
+        return self.nL * self.Pc
+
+    def coords(self, rank: int) -> Tuple[int, int]:
+        return rank // self.Pc, rank % self.Pc
+
+    def rank_of(self, r: int, c: int) -> int:
+        return r * self.Pc + c
+
+    def a_owner(self, j: int) -> int:  # process-column index holding A chunk j
+        return j // (self.chunks // self.Pc)
+
+    def b_owner(self, j: int) -> int:  # process-row index holding B chunk j
+        return j // (self.chunks // self.Pr)
+
+    def a_local_chunk(self, j: int) -> int:
+        return j - self.a_owner(j) * (self.chunks // self.Pc)
+
+    def b_local_chunk(self, j: int) -> int:
+        return j - self.b_owner(j) * (self.chunks // self.Pr)
+
+
+def make_layout(P: int, mL: int, nL: int, K: int, per_owner: int = 2) -> Layout:
+    pr, pc = grid_shape(P)
+    L = pr * pc // math.gcd(pr, pc) * per_owner
+    L = max(L, 1)
+    if K % L:
+        raise ValueError(f"K={K} must be a multiple of the chunk count {L}")
+    return Layout(P, pr, pc, mL, nL, K, L, K // L)
+
+
+class Summa:
+    """The distributed C += A·B over a Layout. Buffers are torch tensors on
+    `device`; `gemm(a_chunk, b_chunk, c)` performs c += a·b with a (mL x KC,
+    ld mL), b (KC x nL, ld KC), c (mL x nL, ld mL), all flat column-major."""
+
+    def __init__(self, lay: Layout, rank: int, device, gemm: Callable, dist=None, row_group=None, col_group=None):
+        import torch
+
+        self.lay, self.rank, self.device, self.gemm = lay, rank, device, gemm
+        self.r, self.c = lay.coords(rank)
+        self.dist = dist
+        self.row_group, self.col_group = row_group, col_group
+        self.abuf = [torch.empty(lay.mL * lay.KC, dtype=torch.float64, device=device) for _ in range(2)]
+        self.bbuf = [torch.empty(lay.KC * lay.nL, dtype=torch.float64, device=device) for _ in range(2)]
+        self.exchanged_bytes = 0
+
+    @staticmethod
+    def groups(dist, lay: Layout):
+        """Row and column sub-communicators (every rank must call, in order)."""
+        rows = [dist.new_group([lay.rank_of(r, c) for c in range(lay.Pc)]) for r in range(lay.Pr)]
+        cols = [dist.new_group([lay.rank_of(r, c) for r in range(lay.Pr)]) for c in range(lay.Pc)]
+        return rows, cols
+
+    def a_chunk_view(self, A_local, j: int):
+        lay = self.lay
+        q = lay.a_local_chunk(j)
+        return A_local[q * lay.mL * lay.KC:(q + 1) * lay.mL * lay.KC]
+
+    def b_chunk_view(self, B_local, j: int):
+        lay = self.lay
+        q = lay.b_local_chunk(j)
+        return B_local[q * lay.KC * lay.nL:(q + 1) * lay.KC * lay.nL]
+
+    def _post(self, A_local, B_local, j: int):
+        """Issue the broadcasts of chunk j; returns (a, b, works)."""
+        lay = self.lay
+        works = []
+        a_src_c, b_src_r = lay.a_owner(j), lay.b_owner(j)
+        a = self.a_chunk_view(A_local, j) if a_src_c == self.c else self.abuf[j % 2]
+        b = self.b_chunk_view(B_local, j) if b_src_r == self.r else self.bbuf[j % 2]
+        if lay.Pc > 1:
+            works.append(self.dist.broadcast(a, src=lay.rank_of(self.r, a_src_c), group=self.row_group,
+                                             async_op=True))
+            if a_src_c != self.c:
+                self.exchanged_bytes += a.numel() * 8
+        if lay.Pr > 1:
+            works.append(self.dist.broadcast(b, src=lay.rank_of(b_src_r, self.c), group=self.col_group,
+                                             async_op=True))
+            if b_src_r != self.r:
+                self.exchanged_bytes += b.numel() * 8
+        return a, b, works
+
+    def run(self, A_local, B_local, C_local) -> None:
+        """C_local += A_r · B_c over all K chunks (ascending k)."""
+        L = self.lay.chunks
+        pending = self._post(A_local, B_local, 0)
+        for j in range(L):
+            a, b, works = pending
+            for w in works:
+                w.wait()  # the compute stream waits on the exchange of chunk j
+            if j + 1 < L:
+                pending = self._post(A_local, B_local, j + 1)  # overlaps the GEMM below
+            self.gemm(a, b, C_local)
+
+
+def fill_local(lay: Layout, rank: int, A_local, B_local, C_local, fill_block, seeds=(11, 12, 13)):
+    """Seeded blocks of the global A (M x K), B (K x N), C (M x N): every
+    rank generates exactly its own pieces from global element indices."""
+    r, c = lay.coords(rank)
+    per_a = lay.chunks // lay.Pc
+    for q in range(per_a):
+        j = c * per_a + q
+        fill_block(A_local[q * lay.mL * lay.KC:(q + 1) * lay.mL * lay.KC], lay.mL, lay.KC, lay.mL, seeds[0],
+                   r * lay.mL, j * lay.KC, lay.M)
+    per_b = lay.chunks // lay.Pr
+    for q in range(per_b):
+        j = r * per_b + q
+        fill_block(B_local[q * lay.KC * lay.nL:(q + 1) * lay.KC * lay.nL], lay.KC, lay.nL, lay.KC, seeds[1],
+                   j * lay.KC, c * lay.nL, lay.K)
+    fill_block(C_local, lay.mL, lay.nL, lay.mL, seeds[2], r * lay.mL, c * lay.nL, lay.M)
+
+
+# ----------------------------------------------------------------- bench
+def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
+    """bench.py at N > 1: weak scaling, each rank owns a size x size block of
+    C with K = size; value = total flops / max-over-ranks time."""
+    import json
+
+    import torch
+    import torch.distributed as dist
+
+    size = args.size
+    lay = make_layout(world, size, size, size)
+    rows, cols = Summa.groups(dist, lay)
+    r, c = lay.coords(rank)
+    dev = torch.device("cuda", local)
+    nest, bs, hier = make_plan(T, lay.mL, lay.nL, lay.KC)
+    A = torch.empty(lay.mL * lay.K // lay.Pc, dtype=torch.float64, device=dev)
+    B = torch.empty(lay.K // lay.Pr * lay.nL, dtype=torch.float64, device=dev)
+    C = torch.empty(lay.mL * lay.nL, dtype=torch.float64, device=dev)
+    fill_local(lay, rank, A, B, C, T.fill_uniform_block)
+    opts = T.ExecOptions(numerics="dmma", schedule="fused")
+
+    def gemm(a, b, cc):
+        T.execute(nest, a, b, cc, opts)
+
+    s = Summa(lay, rank, dev, gemm, dist, rows[r], cols[c])
+    for _ in range(args.warmup):
+        s.run(A, B, C)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.exchanged_bytes = 0
+    e0.record()
+    for _ in range(args.steps):
+        s.run(A, B, C)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    t = float(ms.item()) / 1e3
+    flops = 2.0 * lay.M * lay.N * lay.K * args.steps
+    if rank == 0:
+        print(json.dumps({
+            "metric": "GEMM TFLOP/s (FP64) and % of FP64 peak", "value": flops / t / 1e12, "unit": "TFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based uniform[-1,1), generated per rank from global indices)",
+            "config": {"workload": f"fp64 C+=A*B, C 2-D partitioned {lay.Pr}x{lay.Pc}, local {lay.mL}x{lay.nL}, "
+                                   f"K={lay.K}, family C2A1C0 fused/DMMA", "grid": [lay.Pr, lay.Pc],
+                       "chunks": lay.chunks, "kc": lay.KC, "parallelism": f"2-D C partition {lay.Pr}x{lay.Pc}"},
+            "exchanged_bytes_per_step_rank0": s.exchanged_bytes / args.steps,
+            "gpu_launches": (nest.last_launch()["launches"]) * lay.chunks * args.steps,
+        }))
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

@@ -593,6 +593,16 @@ def fill_uniform_device(x, seed: int, offset: int = 0, stream=None) -> None:
     _check(N.lib().tm_fill_uniform_device(x.data_ptr(), x.numel(), seed, offset, C.c_void_p(st)))
 
 
+def fill_uniform_block(x, rows: int, cols: int, ld: int, seed: int, row0: int, col0: int, global_ld: int,
+                       stream=None) -> None:
+    """x(i, j) = counter-based value of global element (row0+i, col0+j) of a
+    column-major matrix with leading dimension global_ld (CUDA float64)."""
+    import torch
+
+    st = torch.cuda.current_stream().cuda_stream if stream is None else getattr(stream, "cuda_stream", stream)
+    _check(N.lib().tm_fill_uniform_block(x.data_ptr(), rows, cols, ld, seed, row0, col0, global_ld, C.c_void_p(st)))
+
+
 def measure_fp64_peak(launches: int = 20) -> float:
     """Sustained FP64 DMMA TFLOP/s of the current device (roofline denominator)."""
     v = C.c_double(0)
