@@ -86,7 +86,8 @@ typedef struct {
     int32_t schedule;   /* TM_SCHEDULE_* */
     int32_t split_k;    /* fused schedule: k splits per tile, deterministic reduction (1 = none, 0 = auto) */
     int32_t ctas;       /* persistent grid size (0 = SMs x occupancy) */
-    int32_t tile;       /* CTA tile edge: 128 or 64 (0 = auto from the register tile) */
+    int32_t tile;       /* CTA tile rows: 128 or 64 (0 = auto from the register tile) */
+    int32_t tile_n;     /* CTA tile columns (0 = same as tile); 128 x 64 runs two CTAs per SM */
 } tm_exec_opts;
 
 typedef struct tm_plan tm_plan;

@@ -156,9 +156,16 @@ int sm_count() {
 gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o) {
     const bool small_tile = o.tile == 64 || (o.tile == 0 && (nest.m_r < 128 || nest.n_r < 128));
     if (o.tile != 0 && o.tile != 64 && o.tile != 128) fail_usage("tile must be 0, 64 or 128");
+    const int tn = o.tile_n == 0 ? o.tile : o.tile_n;
+    if (o.tile_n != 0 && !((o.tile == 128 && (tn == 64 || tn == 128)) || (o.tile == 64 && tn == 64)))
+        fail_usage("tile x tile_n must be 128x128, 128x64 or 64x64");
     switch (o.numerics) {
-        case TM_NUMERICS_DMMA: return small_tile ? gpu::kDmma64 : gpu::kDmma128;
-        case TM_NUMERICS_FMA: return small_tile ? gpu::kFma64 : gpu::kFma128;
+        case TM_NUMERICS_DMMA:
+            if (o.tile == 128 && tn == 64) return gpu::kDmma128x64;
+            return small_tile ? gpu::kDmma64 : gpu::kDmma128;
+        case TM_NUMERICS_FMA:
+            if (tn == 64 && o.tile == 128) fail_usage("fma numerics run on square tiles");
+            return small_tile ? gpu::kFma64 : gpu::kFma128;
         case TM_NUMERICS_EXACT:
             if (o.tile == 128) fail_usage("exact numerics run on the 64x64 tile only");
             return gpu::kExact64;

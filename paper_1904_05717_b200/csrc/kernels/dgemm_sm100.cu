@@ -502,6 +502,8 @@ const Entry kTable[kKernelCount] = {
      64, 64, 256, smem_of<64, 64, true, kStagesSimt>()},
     {{(const void*)k_simt<128, 128, 8, 8, kStagesSimt, false>, (const void*)k_simt<128, 128, 8, 8, kStagesSimt, false>},
      128, 128, 256, smem_of<128, 128, true, kStagesSimt>()},
+    {{(const void*)k_dmma<128, 64, kBKSmall, 64, 32, kStagesSmall, false>, (const void*)k_dmma<128, 64, kBKSmall, 64, 32, kStagesSmall, true>},
+     128, 64, 128, dmma_smem<128, 64, kBKSmall, kStagesSmall>()},
 };
 
 KernelInfo g_info[kKernelCount];

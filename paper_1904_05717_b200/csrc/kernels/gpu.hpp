@@ -43,7 +43,8 @@ enum Kernel : int {
     kFma64 = 2,     // 64x64, DFMA chain per entry (bit-exact vs sequential fma)
     kExact64 = 3,   // 64x64, DMUL + DADD per step (bit-exact vs the reference)
     kFma128 = 4,    // 128x128, 8x8 per thread DFMA chain
-    kKernelCount = 5
+    kDmma128x64 = 5,  // 128x64 C tile, 4 warps of 64x32, two CTAs per SM (prologue/epilogue overlap)
+    kKernelCount = 6
 };
 
 struct KernelInfo {

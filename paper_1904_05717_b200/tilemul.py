@@ -470,10 +470,12 @@ class ExecOptions:  # exec.hpp:48-53, re-targeted
     schedule: str = "fused"     # fused | faithful
     split_k: int = 1            # fused: k slices with a fixed-order reduction (0 = auto)
     ctas: int = 0               # persistent grid (0 = SMs x occupancy)
-    tile: int = 0               # CTA tile edge 64/128 (0 = from the register tile)
+    tile: int = 0               # CTA tile rows 64/128 (0 = from the register tile)
+    tile_n: int = 0             # CTA tile columns (0 = tile); 128x64 runs two CTAs per SM
 
     def _c(self):
-        return N.tm_exec_opts(NUMERICS[self.numerics], SCHEDULES[self.schedule], self.split_k, self.ctas, self.tile)
+        return N.tm_exec_opts(NUMERICS[self.numerics], SCHEDULES[self.schedule], self.split_k, self.ctas, self.tile,
+                              self.tile_n)
 
 
 class LoopNest:  # plan.hpp:25-85
