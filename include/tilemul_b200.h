@@ -157,6 +157,17 @@ int tm_execute(tm_plan* plan, const double* A, int64_t lda, const double* B, int
  * A, B, C to the device, runs, copies C back; synchronous. Host memory may be
  * pinned (fast path) or pageable. */
 int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts* opts);
+/* Mixed precision on the 5th-generation tensor cores (tcgen05 + TMEM,
+ * BASELINE configs[3]): C(m x n, fp32) += A·B with A, B column-major in BF16
+ * (dtype TM_DTYPE_BF16) or in fp32 holding TF32 values (TM_DTYPE_TF32),
+ * fp32 accumulation. Fused schedule only; bases and leading dimensions must
+ * be 16-byte aligned (TMA). */
+enum { TM_DTYPE_BF16 = 1, TM_DTYPE_TF32 = 2 };
+int tm_execute_tc(tm_plan* plan, int dtype, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
+                  int64_t ldc, const tm_exec_opts* opts, void* stream);
+/* Device rounding of FP64 inputs: to BF16 (RNE; y is uint16 storage) or to
+ * TF32 values in fp32 storage (RNE to 11 significant bits). */
+int tm_round_inputs(int dtype, const double* x, void* y, int64_t count, void* stream);
 /* Number of CTA tasks and kernel launches the last tm_execute issued. */
 int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, int32_t* ctas);
 

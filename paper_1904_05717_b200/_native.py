@@ -72,6 +72,8 @@ SIGNATURES = [
     ("tm_roofline_bound", dbl, [dbl, dbl, dbl]),
     ("tm_execute", C.c_int, [P, P, i64, P, i64, P, i64, C.POINTER(tm_exec_opts), P]),
     ("tm_execute_host", C.c_int, [P, P, P, P, C.POINTER(tm_exec_opts)]),
+    ("tm_execute_tc", C.c_int, [P, C.c_int, P, i64, P, i64, P, i64, C.POINTER(tm_exec_opts), P]),
+    ("tm_round_inputs", C.c_int, [C.c_int, P, P, i64, P]),
     ("tm_plan_last_launch", C.c_int, [P, C.POINTER(i64), C.POINTER(i32), C.POINTER(i32)]),
     ("tm_measure_fp64_peak", C.c_int, [C.c_int, C.POINTER(dbl)]),
     ("tm_fill_uniform_device", C.c_int, [P, i64, C.c_uint64, C.c_uint64, P]),

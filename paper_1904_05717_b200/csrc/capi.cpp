@@ -189,7 +189,10 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
     auto s = std::make_unique<Schedule>();
     s->kernel = kernel;
     gpu::KernelInfo info{};
-    cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
+    if (kernel == gpu::kTcBf16 || kernel == gpu::kTcTf32)
+        info = gpu::KernelInfo{128, 256, 256, gpu::tc_smem_bytes(kernel == gpu::kTcTf32), 1};
+    else
+        cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
     const int slots = sm_count() * std::max(1, info.ctas_per_sm);
     const Extents& e = nest.ext;
     check_i32(e.m, "m");
@@ -215,10 +218,11 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
             const i64 nt = static_cast<i64>(tiles.size());
             if (nt * 2 <= slots) split = static_cast<int>(std::min<i64>(slots / nt, std::max<i64>(1, e.k / 1024)));
         }
-        split = std::max(1, std::min<int>(split, static_cast<int>(cdiv(e.k, 16))));
+        const i64 slab = (kernel == gpu::kTcBf16 || kernel == gpu::kTcTf32) ? 64 : 32;
+        split = std::max(1, std::min<int>(split, static_cast<int>(cdiv(e.k, slab))));
         s->slices = split;
-        // k ranges aligned to the 16-deep slab
-        const i64 per = cdiv(cdiv(e.k, split), 16) * 16;
+        // k ranges aligned to the kernel's k-slab
+        const i64 per = cdiv(cdiv(e.k, split), slab) * slab;
         for (const auto& t : tiles)
             for (int q = 0; q < split; ++q) {
                 const i64 p0 = q * per;
@@ -547,6 +551,44 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
         run(plan, plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, opts, st);
         cuda_check(cudaMemcpyAsync(C, plan->dC, nc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H C");
         cuda_check(cudaStreamSynchronize(st), "execute_host sync");
+    });
+}
+
+int tm_execute_tc(tm_plan* plan, int dtype, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
+                  int64_t ldc, const tm_exec_opts* opts, void* stream) {
+    return guard([&] {
+        if (!plan) fail_usage("null plan");
+        if (!A || !B || !C) fail_usage("null operand pointer");
+        if (dtype != TM_DTYPE_BF16 && dtype != TM_DTYPE_TF32) fail_usage("dtype must be TM_DTYPE_BF16 or TM_DTYPE_TF32");
+        const Extents& e = plan->nest.ext;
+        if (lda < e.m || ldb < e.k || ldc < e.m) fail_usage("leading dimension smaller than the operand's row count");
+        tm_exec_opts o{};
+        if (opts) o = *opts;
+        if (o.schedule != TM_SCHEDULE_FUSED) fail_usage("tensor-core path runs the fused schedule only");
+        if (o.split_k > 1) fail_usage("tensor-core path does not split k");
+        o.split_k = 1;
+        const gpu::Kernel kernel = dtype == TM_DTYPE_TF32 ? gpu::kTcTf32 : gpu::kTcBf16;
+        std::lock_guard<std::mutex> lk(plan->mu);
+        Key key{o.schedule, kernel, 1, o.ctas, false};
+        auto& slot = plan->schedules[key];
+        int dev = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        if (!slot || slot->device != dev) slot = lower(plan->nest, o, kernel);
+        Schedule& s = *slot;
+        cuda_check(gpu::launch_tc(dtype == TM_DTYPE_TF32, A, lda, B, ldb, C, ldc, e.m, e.n, e.k, s.tasks,
+                                  static_cast<int>(s.host_tasks.size()), s.grid, static_cast<cudaStream_t>(stream)),
+                   "tensor-core kernel launch (TMA needs 16-byte aligned bases and leading dimensions)");
+        plan->last_tasks = static_cast<int64_t>(s.host_tasks.size());
+        plan->last_launches = 1;
+        plan->last_ctas = s.grid;
+    });
+}
+
+int tm_round_inputs(int dtype, const double* x, void* y, int64_t count, void* stream) {
+    return guard([&] {
+        if (dtype != TM_DTYPE_BF16 && dtype != TM_DTYPE_TF32) fail_usage("dtype must be TM_DTYPE_BF16 or TM_DTYPE_TF32");
+        cuda_check(gpu::launch_round(dtype == TM_DTYPE_TF32, x, y, count, static_cast<cudaStream_t>(stream)),
+                   "round launch");
     });
 }
 

@@ -44,7 +44,9 @@ enum Kernel : int {
     kExact64 = 3,   // 64x64, DMUL + DADD per step (bit-exact vs the reference)
     kFma128 = 4,    // 128x128, 8x8 per thread DFMA chain
     kDmma128x64 = 5,  // 128x64 C tile, 4 warps of 64x32, two CTAs per SM (prologue/epilogue overlap)
-    kKernelCount = 6
+    kKernelCount = 6,
+    kTcBf16 = 100,    // tcgen05 BF16 inputs, fp32 TMEM accumulate, 128x256 tile (tc_gemm_sm100.cu)
+    kTcTf32 = 101     // tcgen05 TF32 inputs
 };
 
 struct KernelInfo {
@@ -63,6 +65,12 @@ cudaError_t launch_reduce(double* C, int64_t ldc, const double* work, int64_t wo
                           int slices, int64_t m, int64_t n, cudaStream_t stream);
 // Sustained FP64 DMMA rate of this device (TFLOP/s) over `launches` probe launches.
 cudaError_t measure_fp64_peak(int launches, double* tflops);
+// tcgen05 BF16/TF32-input GEMM over a task list (C fp32, column-major).
+cudaError_t launch_tc(bool tf32, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
+                      int64_t m, int64_t n, int64_t k, const Task* tasks, int ntasks, int grid, cudaStream_t stream);
+// fp64 -> bf16 (RNE) or fp64 -> tf32-valued fp32 (RNE to 11 significant bits).
+cudaError_t launch_round(bool tf32, const double* x, void* y, int64_t count, cudaStream_t stream);
+int tc_smem_bytes(bool tf32);
 cudaError_t launch_fill_block(double* x, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
                               int64_t col0, int64_t gld, cudaStream_t stream);
 cudaError_t launch_fill(double* x, int64_t count, uint64_t seed, uint64_t offset, cudaStream_t stream);

@@ -1,0 +1,382 @@
+// BF16 / TF32-input C(fp32) += A·B on the 5th-generation tensor cores
+// (tcgen05 + TMEM), BASELINE.json configs[3]. sm_100a only.
+//
+// Same task model as the FP64 kernels (gpu.hpp): a persistent grid walks the
+// lowered task list; each task is one 128 x 256 C tile over a k range.
+// Warp roles (256 threads):
+//   warp 0      TMA producer: A (column-major = M-major) and B (column-major =
+//               K-major) k-slabs -> 128B-swizzled shared memory, 4-stage ring
+//               of full/empty mbarriers;
+//   warp 1      MMA issuer: one thread issues tcgen05.mma (M=128, N=256,
+//               K=32 bytes) into a TMEM accumulator, commits to the ring's
+//               empty barriers and, per tile, to the accumulator-full barrier;
+//   warp 2      TMEM allocator (512 columns = two 256-column accumulators);
+//   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns per warp, C += acc
+//               with coalesced fp32 column accesses, then release the
+//               accumulator so the next tile's MMAs overlap this epilogue.
+// The SMEM level of the MOMMS member is the TMA ring; the register level is
+// the TMEM accumulator (128 x 256 fp32 per tile).
+#include <cstdint>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "gpu.hpp"
+
+namespace mmm {
+namespace gpu {
+namespace {
+
+constexpr int kTcStages = 4;
+constexpr int kTcBM = 128, kTcBN = 256;
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "TC_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra TC_DONE;\n\t"
+        "bra TC_WAIT;\n"
+        "TC_DONE:\n\t}\n" ::"r"(saddr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::
+            "r"(saddr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(saddr(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// Shared-memory matrix descriptor (SM100 UMMA): start, LBO, SBO in 16-byte
+// units, version 1, layout type 2 = SWIZZLE_128B (16-byte atoms, 8-row
+// period) or 1 = SWIZZLE_128B_BASE32B (32-byte atoms, 4-row period; the only
+// M-major layout tf32 operands accept).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
+    return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+           (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) |
+           (static_cast<uint64_t>(layout) << 61);
+}
+
+// Instruction descriptor: D fp32, A/B format (BF16 = 1, TF32 = 2), A M-major,
+// B K-major, N = 256, M = 128.
+template <bool TF32>
+__host__ __device__ constexpr uint32_t instr_desc() {
+    return (1u << 4) | ((TF32 ? 2u : 1u) << 7) | ((TF32 ? 2u : 1u) << 10) | (1u << 15) | (0u << 16) |
+           (static_cast<uint32_t>(kTcBN >> 3) << 17) | (static_cast<uint32_t>(kTcBM >> 4) << 24);
+}
+
+template <bool TF32>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+    if constexpr (TF32) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(saddr(bar))
+                 : "memory");
+}
+
+#define TC_LD32(taddr, r)                                                                                           \
+    asm volatile(                                                                                                   \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"                                            \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),          \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),    \
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),  \
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])   \
+        : "r"(taddr))
+
+struct TcArgs {
+    float* C;
+    int64_t ldc;
+    const Task* tasks;
+    int32_t ntasks;
+};
+
+template <bool TF32>
+struct TcGeo {
+    static constexpr int E = TF32 ? 4 : 2;     // bytes per input element
+    static constexpr int BK = 128 / E;          // k per stage: one 128-byte swizzle row of K-major B
+    static constexpr int MATOM = 128 / E;       // m per 128-byte row of M-major A
+    static constexpr int A_BOXES = kTcBM / MATOM;
+    static constexpr int A_BOX_BYTES = 128 * BK;
+    static constexpr int A_BYTES = kTcBM * BK * E;
+    static constexpr int B_BYTES = kTcBN * BK * E;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int UK = 32 / E;           // k per MMA instruction
+    static constexpr int NMMA = BK / UK;
+    // M-major A: bf16 uses SWIZZLE_128B (8-row groups), tf32 SWIZZLE_128B_BASE32B (4-row groups)
+    static constexpr uint32_t A_LAYOUT = TF32 ? 1u : 2u;
+    static constexpr uint32_t A_SBO = TF32 ? 512u : 1024u;
+    static constexpr int SMEM = kTcStages * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <bool TF32>
+__global__ void __launch_bounds__(256, 1) k_tc(const __grid_constant__ CUtensorMap tmA,
+                                               const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+    using G = TcGeo<TF32>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * G::STAGE);
+    uint64_t* empty = full + kTcStages;
+    uint64_t* tfull = empty + kTcStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(saddr(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int ti = blockIdx.x; ti < a.ntasks; ti += gridDim.x) {
+                const Task t = a.tasks[ti];
+                const int nk = (t.k + G::BK - 1) / G::BK;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * G::STAGE;
+                    uint8_t* sb = sa + G::A_BYTES;
+                    mbar_expect_tx(&full[stage], G::STAGE);
+                    const int kc = t.p0 + kb * G::BK;
+#pragma unroll
+                    for (int h = 0; h < G::A_BOXES; ++h)
+                        tma_load_2d(sa + h * G::A_BOX_BYTES, &tmA, &full[stage], t.i0 + h * G::MATOM, kc);
+                    tma_load_2d(sb, &tmB, &full[stage], kc, t.j0);
+                    if (++stage == kTcStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            constexpr uint32_t idesc = instr_desc<TF32>();
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t aphase = 0;
+            for (int ti = blockIdx.x; ti < a.ntasks; ti += gridDim.x) {
+                const Task t = a.tasks[ti];
+                const int nk = (t.k + G::BK - 1) / G::BK;
+                mbar_wait(&tempty[acc], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * kTcBN);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = saddr(smem + stage * G::STAGE);
+                    const uint32_t sb = sa + G::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < G::NMMA; ++kk) {
+                        // A: M-major SW128 — LBO = next 128-byte M chunk (one TMA box), SBO = next 8 k rows.
+                        const uint64_t da = smem_desc(sa + kk * G::UK * 128, G::A_BOX_BYTES, G::A_SBO, G::A_LAYOUT);
+                        // B: K-major SW128 — advance 32 bytes of k inside the swizzled row, SBO = 8 n rows.
+                        const uint64_t db = smem_desc(sb + kk * 32, 16, 1024);
+                        umma<TF32>(tmem_d, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == kTcStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    aphase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue
+        const int ew = warp - 4;
+        const int row = ew * 32 + lane;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int ti = blockIdx.x; ti < a.ntasks; ti += gridDim.x) {
+            const Task t = a.tasks[ti];
+            mbar_wait(&tfull[acc], aphase);
+            tc_fence_after();
+            const bool live = row < t.m;
+            float* crow = a.C + (static_cast<int64_t>(t.i0) + row) + static_cast<int64_t>(t.j0) * a.ldc;
+#pragma unroll 1
+            for (int cb = 0; cb < kTcBN / 32; ++cb) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) +
+                                       static_cast<uint32_t>(acc * kTcBN + cb * 32);
+                TC_LD32(taddr, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                if (live) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = cb * 32 + j;
+                        if (col < t.n) {
+                            float* p = crow + static_cast<int64_t>(col) * a.ldc;
+                            *p = *p + __uint_as_float(r[j]);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                aphase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+cudaError_t encoder() {
+    if (g_encode) return cudaSuccess;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess) return e;
+    if (q != cudaDriverEntryPointSuccess || fn == nullptr) return cudaErrorNotSupported;
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    return cudaSuccess;
+}
+
+// 2-D column-major tensor map: dim0 contiguous (rows), box {box0, box1}, 128B swizzle.
+cudaError_t make_map(CUtensorMap* m, const void* base, bool tf32, int64_t rows, int64_t cols, int64_t ld, int box0,
+                     int box1, CUtensorMapSwizzle swz) {
+    const int E = tf32 ? 4 : 2;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * E};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box0), static_cast<cuuint32_t>(box1)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(m, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                          const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <bool TF32>
+cudaError_t launch_tc_t(const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc, int64_t m,
+                        int64_t n, int64_t k, const Task* tasks, int ntasks, int grid, cudaStream_t stream) {
+    using G = TcGeo<TF32>;
+    cudaError_t e = encoder();
+    if (e != cudaSuccess) return e;
+    if ((lda * G::E) % 16 || (ldb * G::E) % 16 || reinterpret_cast<uintptr_t>(A) % 16 ||
+        reinterpret_cast<uintptr_t>(B) % 16)
+        return cudaErrorInvalidValue;  // TMA: 16-byte aligned bases and row strides
+    CUtensorMap ma, mb;
+    if ((e = make_map(&ma, A, TF32, m, k, lda, G::MATOM, G::BK,
+                      TF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess)
+        return e;
+    if ((e = make_map(&mb, B, TF32, k, n, ldb, G::BK, kTcBN, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
+    static bool attr[2] = {false, false};
+    if (!attr[TF32]) {
+        if ((e = cudaFuncSetAttribute(k_tc<TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM)) != cudaSuccess)
+            return e;
+        attr[TF32] = true;
+    }
+    TcArgs args{C, ldc, tasks, ntasks};
+    k_tc<TF32><<<grid, 256, G::SMEM, stream>>>(ma, mb, args);
+    return cudaGetLastError();
+}
+
+// Round fp64 values to bf16 (RNE) or to tf32-in-fp32 (RNE to 10 mantissa bits).
+__global__ void k_round_bf16(const double* x, uint16_t* y, int64_t count) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        // exact RNE of the double to 8 significant bits (bf16), no double rounding via fp32
+        int ex;
+        const double mant = frexp(x[i], &ex);  // x = mant * 2^ex, 0.5 <= |mant| < 1
+        const float r = static_cast<float>(ldexp(rint(ldexp(mant, 8)), ex - 8));
+        y[i] = static_cast<uint16_t>(__float_as_uint(r) >> 16);
+    }
+}
+__global__ void k_round_tf32(const double* x, float* y, int64_t count) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int ex;
+        const double mant = frexp(x[i], &ex);
+        const double q = rint(ldexp(mant, 11));       // tf32: 10 stored + implicit = 11 significant bits
+        y[i] = static_cast<float>(ldexp(q, ex - 11));
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_tc(bool tf32, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
+                      int64_t m, int64_t n, int64_t k, const Task* tasks, int ntasks, int grid, cudaStream_t stream) {
+    if (ntasks <= 0) return cudaSuccess;
+    return tf32 ? launch_tc_t<true>(A, lda, B, ldb, C, ldc, m, n, k, tasks, ntasks, grid, stream)
+                : launch_tc_t<false>(A, lda, B, ldb, C, ldc, m, n, k, tasks, ntasks, grid, stream);
+}
+
+cudaError_t launch_round(bool tf32, const double* x, void* y, int64_t count, cudaStream_t stream) {
+    if (count <= 0) return cudaSuccess;
+    const int blocks = static_cast<int>(std::min<int64_t>((count + 255) / 256, 148 * 32));
+    if (tf32)
+        k_round_tf32<<<blocks, 256, 0, stream>>>(x, static_cast<float*>(y), count);
+    else
+        k_round_bf16<<<blocks, 256, 0, stream>>>(x, static_cast<uint16_t*>(y), count);
+    return cudaGetLastError();
+}
+
+int tc_smem_bytes(bool tf32) { return tf32 ? TcGeo<true>::SMEM : TcGeo<false>::SMEM; }
+
+}  // namespace gpu
+}  // namespace mmm

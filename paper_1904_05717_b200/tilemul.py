@@ -587,6 +587,38 @@ def execute(nest: LoopNest, A, B, C_, opts: ExecOptions = None, stream=None) -> 
         raise ValueError("operands must be all on the device or all on the host")
 
 
+DTYPES = {"bf16": 1, "tf32": 2}
+
+
+def execute_tc(nest: LoopNest, A, B, C_, dtype: str = "bf16", opts: ExecOptions = None, stream=None) -> None:
+    """C (fp32) += A·B on the tcgen05 tensor cores. A, B: CUDA tensors,
+    column-major flat (bf16 as torch.bfloat16/int16 storage, tf32 as float32
+    holding TF32 values). Fused schedule."""
+    import torch
+
+    opts = opts or ExecOptions()
+    s = nest.shape
+    for x, n_, name in ((A, s.m * s.k, "A"), (B, s.k * s.n, "B"), (C_, s.m * s.n, "C")):
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.numel() == n_ and x.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous CUDA tensor of {n_} elements")
+    if C_.dtype != torch.float32:
+        raise ValueError("C must be float32")
+    st = torch.cuda.current_stream().cuda_stream if stream is None else getattr(stream, "cuda_stream", stream)
+    o = opts._c()
+    _check(N.lib().tm_execute_tc(nest._ptr, DTYPES[dtype], A.data_ptr(), s.m, B.data_ptr(), s.k, C_.data_ptr(), s.m,
+                                 C.byref(o), C.c_void_p(st)))
+
+
+def round_inputs(x, dtype: str, stream=None):
+    """FP64 CUDA tensor -> bf16 (returned as torch.bfloat16) or TF32-valued float32, RNE."""
+    import torch
+
+    y = torch.empty(x.numel(), dtype=torch.bfloat16 if dtype == "bf16" else torch.float32, device=x.device)
+    st = torch.cuda.current_stream().cuda_stream if stream is None else getattr(stream, "cuda_stream", stream)
+    _check(N.lib().tm_round_inputs(DTYPES[dtype], x.data_ptr(), y.data_ptr(), x.numel(), C.c_void_p(st)))
+    return y
+
+
 def fill_uniform_device(x, seed: int, offset: int = 0, stream=None) -> None:
     """Counter-based uniform[-1,1) fill of a CUDA float64 tensor."""
     import torch

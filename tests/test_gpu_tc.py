@@ -1,0 +1,83 @@
+"""GPU parity of the tcgen05 mixed-precision path (BASELINE configs[3]):
+BF16 or TF32 inputs rounded from uniform[-1,1) FP64 values, FP32 accumulate,
+checked against the FP64 oracle of the ROUNDED inputs with the bound
+|C - C_ref| <= (k+2)·u·(|A||B| + |C0|)_ij, u = 2^-24 (fp32 accumulation;
+tensor-core accumulation order is unspecified, so no bitwise claim)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1904_05717_b200 import tilemul as T
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+U32 = 2.0 ** -24
+
+
+def tc_plan(m, n, k):
+    # register tile = the TMEM accumulator (128 x 256 fp32); capacities in 2-byte elements
+    hier = T.CacheHierarchy.from_capacities([128 * 512, 232448 // 2, 132644864 // 2])
+    d = T.parse_name("C2A1C0")
+    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(128, 256)),
+                             pinned=T.BlocksizeSet({(1, "m"): min(128, m)}))
+    return T.build_plan(d, bs, hier, T.Shape(m, n, k))
+
+
+def run_case(m, n, k, dtype, sample=None, seed=5):
+    nest = tc_plan(m, n, k)
+    A64 = torch.empty(m * k, dtype=torch.float64, device="cuda")
+    B64 = torch.empty(k * n, dtype=torch.float64, device="cuda")
+    T.fill_uniform_device(A64, seed)
+    T.fill_uniform_device(B64, seed + 1)
+    A = T.round_inputs(A64, dtype)
+    B = T.round_inputs(B64, dtype)
+    C0 = torch.empty(m * n, dtype=torch.float64, device="cuda")
+    T.fill_uniform_device(C0, seed + 2)
+    C = C0.float()
+    c0 = C.double().cpu().numpy()
+    T.execute_tc(nest, A, B, C, dtype)
+    torch.cuda.synchronize()
+    got = C.double().cpu().numpy()
+    a = A.double().cpu().numpy()
+    b = B.double().cpu().numpy()
+    # rounding is exact RNE: the rounded values differ from the fp64 originals by <= half an ulp
+    ulp = 2.0 ** -8 if dtype == "bf16" else 2.0 ** -11
+    assert np.all(np.abs(a - A64.cpu().numpy()) <= ulp * np.abs(A64.cpu().numpy()) + 1e-300)
+    rng = np.random.default_rng(seed)
+    if sample is None:
+        ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+        ii, jj = ii.ravel(), jj.ravel()
+    else:
+        ii, jj = rng.integers(0, m, sample), rng.integers(0, n, sample)
+    want, ab = O.entries(k, a, m, b, k, c0, m, ii, jj)
+    idx = ii + jj * m
+    bound = (k + 2) * U32 * (ab + np.abs(c0[idx]))
+    err = np.abs(got[idx] - want)
+    assert np.all(err <= bound), f"worst {float(np.max(err / bound)):.3g} of bound"
+    return nest
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+@pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 1024), (136, 264, 520), (1000, 776, 328)])
+def test_tc_small_full_check(dtype, shape):
+    run_case(*shape, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_tc_large_sampled(dtype):
+    nest = run_case(4096, 4096, 4096, dtype, sample=2048)
+    assert nest.last_launch()["tasks"] == (4096 // 128) * (4096 // 256)
+
+
+def test_tc_rejects_unaligned_and_faithful():
+    nest = tc_plan(130, 256, 64)  # lda = 130 bf16 = 260 bytes: not 16-byte aligned for TMA
+    A = torch.zeros(130 * 64, dtype=torch.bfloat16, device="cuda")
+    B = torch.zeros(64 * 256, dtype=torch.bfloat16, device="cuda")
+    C = torch.zeros(130 * 256, dtype=torch.float32, device="cuda")
+    with pytest.raises(T.CudaError):
+        T.execute_tc(nest, A, B, C, "bf16")
+    nest = tc_plan(128, 256, 64)
+    with pytest.raises(ValueError):
+        T.execute_tc(nest, A[:128 * 64], B, C[:128 * 256], "bf16", T.ExecOptions(schedule="faithful"))
