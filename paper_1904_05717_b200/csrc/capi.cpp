@@ -133,14 +133,20 @@ struct tm_plan {
     std::mutex mu;
     // host-buffer execution
     double *dA = nullptr, *dB = nullptr, *dC = nullptr;
-    cudaStream_t host_stream = nullptr;
+    cudaStream_t host_stream = nullptr, copy_stream = nullptr;
+    std::vector<cudaEvent_t> chunk_ready;
+    // k-chunk sub-plans of the host-buffer pipeline (same family and
+    // blocksizes, k extent = one chunk / the tail chunk)
+    std::unique_ptr<tm_plan> chunk_full, chunk_tail;
     int64_t last_tasks = 0;
     int32_t last_launches = 0, last_ctas = 0;
     ~tm_plan() {
         if (dA) cudaFree(dA);
         if (dB) cudaFree(dB);
         if (dC) cudaFree(dC);
+        for (auto ev : chunk_ready) cudaEventDestroy(ev);
         if (host_stream) cudaStreamDestroy(host_stream);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
     }
 };
 
@@ -185,7 +191,7 @@ void check_i32(i64 v, const char* what) {
     if (v > INT32_MAX) fail_usage(std::string(what) + " exceeds the 32-bit task range");
 }
 
-std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel) {
+std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, cudaStream_t stream) {
     auto s = std::make_unique<Schedule>();
     s->kernel = kernel;
     gpu::KernelInfo info{};
@@ -288,7 +294,12 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
     s->grid = std::max(1, std::min<int>(grid, static_cast<int>(T.size())));
     cuda_check(cudaGetDevice(&s->device), "cudaGetDevice");
     cuda_check(cudaMalloc(&s->tasks, sizeof(gpu::Task) * std::max<std::size_t>(1, T.size())), "cudaMalloc(tasks)");
-    cuda_check(cudaMemcpy(s->tasks, T.data(), sizeof(gpu::Task) * T.size(), cudaMemcpyHostToDevice), "upload tasks");
+    // Stream-ordered upload, completed before the schedule is used: a plain
+    // cudaMemcpy from pageable memory may return before the DMA lands, and the
+    // launch streams are non-blocking (no ordering with the legacy stream).
+    cuda_check(cudaMemcpyAsync(s->tasks, T.data(), sizeof(gpu::Task) * T.size(), cudaMemcpyHostToDevice, stream),
+               "upload tasks");
+    cuda_check(cudaStreamSynchronize(stream), "upload tasks (sync)");
     return s;
 }
 
@@ -311,7 +322,7 @@ void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t l
     auto& slot = plan->schedules[key];
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    if (!slot || slot->device != dev) slot = lower(plan->nest, o, kernel);
+    if (!slot || slot->device != dev) slot = lower(plan->nest, o, kernel, stream);
     Schedule& s = *slot;
     const bool vec16 = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(B) % 16 == 0) && origins_even(s.host_tasks);
@@ -545,10 +556,71 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
             cuda_check(cudaMalloc(&plan->dC, nc * sizeof(double)), "cudaMalloc(C)");
         }
         cudaStream_t st = plan->host_stream;
-        cuda_check(cudaMemcpyAsync(plan->dA, A, na * sizeof(double), cudaMemcpyHostToDevice, st), "H2D A");
-        cuda_check(cudaMemcpyAsync(plan->dB, B, nb * sizeof(double), cudaMemcpyHostToDevice, st), "H2D B");
-        cuda_check(cudaMemcpyAsync(plan->dC, C, nc * sizeof(double), cudaMemcpyHostToDevice, st), "H2D C");
-        run(plan, plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, opts, st);
+        tm_exec_opts o{};
+        if (opts) o = *opts;
+        // Pipeline: C first, then A and B in k-chunks on a copy stream, each
+        // chunk's GEMM on the compute stream as soon as its operands landed.
+        // Chunks are multiples of the 32-deep slab and run in ascending k, so
+        // every C entry sees exactly the unchunked operation sequence.
+        const int nchunks = (o.schedule == TM_SCHEDULE_FUSED && o.split_k <= 1 && e.k >= 4096)
+                                ? static_cast<int>(std::min<i64>(8, e.k / 2048))
+                                : 1;
+        if (nchunks == 1) {
+            cuda_check(cudaMemcpyAsync(plan->dA, A, na * sizeof(double), cudaMemcpyHostToDevice, st), "H2D A");
+            cuda_check(cudaMemcpyAsync(plan->dB, B, nb * sizeof(double), cudaMemcpyHostToDevice, st), "H2D B");
+            cuda_check(cudaMemcpyAsync(plan->dC, C, nc * sizeof(double), cudaMemcpyHostToDevice, st), "H2D C");
+            run(plan, plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, opts, st);
+        } else {
+            const i64 kc = cdiv(cdiv(e.k, nchunks), 32) * 32;
+            const int nq = static_cast<int>(cdiv(e.k, kc));
+            const i64 ktail = e.k - (nq - 1) * kc;
+            auto sub = [&](std::unique_ptr<tm_plan>& slot, i64 kk) -> tm_plan* {
+                if (!slot || slot->nest.ext.k != kk) {
+                    slot = std::make_unique<tm_plan>();
+                    slot->nest = plan->nest;
+                    slot->nest.ext.k = kk;
+                    slot->hier = plan->hier;
+                }
+                return slot.get();
+            };
+            tm_plan* pf = sub(plan->chunk_full, kc);
+            tm_plan* pt = ktail == kc ? pf : sub(plan->chunk_tail, ktail);
+            if (!plan->copy_stream)
+                cuda_check(cudaStreamCreateWithFlags(&plan->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            while (static_cast<int>(plan->chunk_ready.size()) < nq) {
+                cudaEvent_t ev;
+                cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+                plan->chunk_ready.push_back(ev);
+            }
+            cudaStream_t cs = plan->copy_stream;
+            cuda_check(cudaMemcpyAsync(plan->dC, C, nc * sizeof(double), cudaMemcpyHostToDevice, cs), "H2D C");
+            for (int q = 0; q < nq; ++q) {
+                const i64 p0 = q * kc, kq = q + 1 == nq ? ktail : kc;
+                cuda_check(cudaMemcpyAsync(plan->dA + p0 * e.m, A + p0 * e.m,
+                                           static_cast<std::size_t>(kq * e.m) * sizeof(double),
+                                           cudaMemcpyHostToDevice, cs),
+                           "H2D A chunk");
+                cuda_check(cudaMemcpy2DAsync(plan->dB + p0, static_cast<std::size_t>(e.k) * sizeof(double), B + p0,
+                                             static_cast<std::size_t>(e.k) * sizeof(double),
+                                             static_cast<std::size_t>(kq) * sizeof(double),
+                                             static_cast<std::size_t>(e.n), cudaMemcpyHostToDevice, cs),
+                           "H2D B chunk");
+                cuda_check(cudaEventRecord(plan->chunk_ready[static_cast<std::size_t>(q)], cs), "event record");
+            }
+            int64_t tasks = 0;
+            int32_t launches = 0;
+            for (int q = 0; q < nq; ++q) {
+                const i64 p0 = q * kc;
+                cuda_check(cudaStreamWaitEvent(st, plan->chunk_ready[static_cast<std::size_t>(q)], 0), "wait chunk");
+                tm_plan* pq = q + 1 == nq ? pt : pf;
+                run(pq, plan->dA + p0 * e.m, e.m, plan->dB + p0, e.k, plan->dC, e.m, &o, st);
+                tasks += pq->last_tasks;
+                launches += pq->last_launches;
+            }
+            plan->last_tasks = tasks;
+            plan->last_launches = launches;
+            plan->last_ctas = pf->last_ctas;
+        }
         cuda_check(cudaMemcpyAsync(C, plan->dC, nc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H C");
         cuda_check(cudaStreamSynchronize(st), "execute_host sync");
     });
@@ -573,7 +645,7 @@ int tm_execute_tc(tm_plan* plan, int dtype, const void* A, int64_t lda, const vo
         auto& slot = plan->schedules[key];
         int dev = 0;
         cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-        if (!slot || slot->device != dev) slot = lower(plan->nest, o, kernel);
+        if (!slot || slot->device != dev) slot = lower(plan->nest, o, kernel, static_cast<cudaStream_t>(stream));
         Schedule& s = *slot;
         cuda_check(gpu::launch_tc(dtype == TM_DTYPE_TF32, A, lda, B, ldb, C, ldc, e.m, e.n, e.k, s.tasks,
                                   static_cast<int>(s.host_tasks.size()), s.grid, static_cast<cudaStream_t>(stream)),

@@ -502,8 +502,8 @@ class LoopNest:  # plan.hpp:25-85
 
     def __del__(self):
         p = getattr(self, "_ptr", None)
-        if p is not None and p.value:
-            N.lib().tm_plan_destroy(p)
+        if p is not None and p.value and N is not None and N._lib is not None:
+            N._lib.tm_plan_destroy(p)
             self._ptr = None
 
     def cell_count(self) -> int:

@@ -213,3 +213,92 @@ def test_large_shapes_sampled_entries(shape, name, split):
     lhs = (Cd.view(n, m).t() - torch.from_numpy(c0).cuda().view(n, m).t()) @ ones
     rhs = A.view(k, m).t() @ (B.view(n, k).t() @ ones)
     assert torch.allclose(lhs, rhs, rtol=0, atol=1e-9 * float(rhs.abs().max()) + 1e-9)
+
+
+# --- host-buffer path (the reference's calling convention): the k-chunked
+# copy/compute pipeline gives bitwise the device-path result -----------------
+@pytest.mark.parametrize("numerics", ["dmma", "exact"])
+def test_host_buffer_pipeline_matches_device_path(numerics):
+    m, n, k = 520, 392, 8224  # k >= 4096 -> 4 chunks of 2080 (multiple of 32), tail 1984
+    hier = T.gpu_hierarchy(128)
+    d = T.parse_name("C2A1C0")
+    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(128, 128)),
+                             pinned=T.BlocksizeSet({(1, "m"): 128}))
+    nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+    a, b, c = O.fill_uniform(31, [(m, k), (k, n), (m, n)])
+    dev_out = run_gpu(nest, a, b, c, numerics=numerics)
+    host_c = c.copy()
+    T.execute(nest, a, b, host_c, T.ExecOptions(numerics=numerics))
+    assert nest.last_launch()["launches"] == 4
+    assert np.array_equal(host_c.view(np.uint64), dev_out.view(np.uint64))
+    if numerics == "exact":
+        want = c.copy()
+        O.execute_nest(m, n, k, [(L.dim, L.blocksize) for L in nest.loops], nest.m_r, nest.n_r, a, b, want)
+        assert np.array_equal(host_c.view(np.uint64), want.view(np.uint64))
+
+
+def test_device_then_pinned_host_on_fresh_plan():
+    """Regression: the task-list upload must be stream-ordered (a pageable
+    cudaMemcpy could return before the DMA landed while pinned copies kept
+    the copy engine busy -> kernels read a half-written task list)."""
+    m = n = 2048
+    k = 8192
+    hier = T.gpu_hierarchy(128)
+    d = T.parse_name("C2A1C0")
+    mk = lambda: T.build_plan(d, T.derive_blocksizes(d, hier, T.Shape(m, n, k),  # noqa: E731
+                                                     opts=T.DeriveOptions(micro=T.MicroTile(128, 128)),
+                                                     pinned=T.BlocksizeSet({(1, "m"): 128})), hier, T.Shape(m, n, k))
+    A = torch.empty(m * k, dtype=torch.float64, device="cuda")
+    B = torch.empty(k * n, dtype=torch.float64, device="cuda")
+    Cd = torch.empty(m * n, dtype=torch.float64, device="cuda")
+    T.fill_uniform_device(A, 1)
+    T.fill_uniform_device(B, 2)
+    T.fill_uniform_device(Cd, 3)
+    Ah, Bh, Ch = (x.cpu().pin_memory().numpy() for x in (A, B, Cd))
+    T.execute(mk(), A, B, Cd)
+    torch.cuda.synchronize()
+    T.execute(mk(), Ah, Bh, Ch)
+    assert np.array_equal(Ch, Cd.cpu().numpy())
+
+
+def test_multigpu_driver_world1_nccl():
+    """The SUMMA driver on the real GPU with an NCCL group of one rank: the
+    chunked local GEMMs over the chunk-major B layout reproduce the product."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1904_05717_b200 import multigpu as MG
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        lay = MG.make_layout(1, 384, 256, 4096)
+        A = torch.empty(lay.mL * lay.K, dtype=torch.float64, device="cuda")
+        B = torch.empty(lay.K * lay.nL, dtype=torch.float64, device="cuda")
+        Cd = torch.empty(lay.mL * lay.nL, dtype=torch.float64, device="cuda")
+        MG.fill_local(lay, 0, A, B, Cd, T.fill_uniform_block)
+        c0 = Cd.cpu().numpy().copy()
+        import bench
+
+        nest, _, _ = bench.make_plan(T, lay.mL, lay.nL, lay.KC)
+        rows, cols = MG.Summa.groups(dist, lay)
+        MG.Summa(lay, 0, torch.device("cuda"), lambda a, b, c: T.execute(nest, a, b, c), dist, rows[0],
+                 cols[0]).run(A, B, Cd)
+        torch.cuda.synchronize()
+        got = Cd.cpu().numpy()
+        rng = np.random.default_rng(1)
+        ii, jj = rng.integers(0, lay.mL, 256), rng.integers(0, lay.nL, 256)
+        p = np.arange(lay.K)
+        a_rows = O.counter_uniform(11, (ii[:, None] + p[None, :] * lay.M).astype(np.uint64))
+        b_cols = O.counter_uniform(12, (p[None, :] + jj[:, None] * lay.K).astype(np.uint64))
+        want = c0[ii + jj * lay.mL] + np.einsum("tp,tp->t", a_rows, b_cols)
+        ab = np.einsum("tp,tp->t", np.abs(a_rows), np.abs(b_cols))
+        ok, worst = H.entrywise_ok(got[ii + jj * lay.mL], want, ab, lay.K, c0=c0[ii + jj * lay.mL])
+        assert ok, worst
+    finally:
+        dist.destroy_process_group()

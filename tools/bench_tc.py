@@ -1,0 +1,64 @@
+#!/usr/bin/env python
+"""Config 4 (BASELINE configs[3]): m=n=k=16384, BF16 / TF32 inputs rounded
+from uniform[-1,1), FP32 accumulate on tcgen05, C (fp32) = 0 initially.
+Times the task kernel with CUDA events (warm-up 2, median of 5) and reports
+TFLOP/s against MEASURED_PEAKS.json's bf16 figure (tf32: half of it, the
+nominal dense ratio, stated)."""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+
+    from paper_1904_05717_b200 import tilemul as T
+
+    size = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
+    m = n = k = size
+    hier = T.CacheHierarchy.from_capacities([128 * 512, 232448 // 2, 132644864 // 2])
+    d = T.parse_name("C2A1C0")
+    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(128, 256)),
+                             pinned=T.BlocksizeSet({(1, "m"): 128, (2, "m"): 1536, (2, "n"): 3072}))
+    nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+    A64 = torch.empty(m * k, dtype=torch.float64, device="cuda")
+    B64 = torch.empty(k * n, dtype=torch.float64, device="cuda")
+    T.fill_uniform_device(A64, 1)
+    T.fill_uniform_device(B64, 2)
+    for dtype in ("bf16", "tf32"):
+        A = T.round_inputs(A64, dtype)
+        B = T.round_inputs(B64, dtype)
+        C = torch.zeros(m * n, dtype=torch.float32, device="cuda")
+        for _ in range(2):
+            T.execute_tc(nest, A, B, C, dtype)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            T.execute_tc(nest, A, B, C, dtype)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        t = statistics.median(ts)
+        tf = 2.0 * m * n * k / t / 1e12
+        peak = peaks["bf16_tflops"] if dtype == "bf16" else peaks["bf16_tflops"] / 2
+        print(json.dumps({"config": "config4", "dtype": dtype, "shape": [m, n, k], "seconds": t, "tflops": tf,
+                          "peak_tflops": peak,
+                          "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" + (" / 2 (nominal tf32:bf16 dense ratio)" if dtype == "tf32" else ""),
+                          "frac": tf / peak, "cta_tile": "128x256 (cta_group::1)",
+                          "blocksizes": {f"{lv}:{dd}": v for (lv, dd), v in bs.entries()},
+                          "launch": nest.last_launch()}), flush=True)
+        del A, B, C
+
+
+if __name__ == "__main__":
+    main()
