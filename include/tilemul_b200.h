@@ -175,6 +175,10 @@ int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, 
  * from `launches` ~7 ms probe launches: the roofline denominator. */
 int tm_measure_fp64_peak(int launches, double* tflops);
 
+/* The reference `run` command's inputs on the host (tools/tilemul_main.cpp:236-242):
+ * mt19937_64(seed), uniform(-1,1), filling A, then B, then C (C may be NULL). */
+int tm_fill_seeded(uint64_t seed, double* a, int64_t na, double* b, int64_t nb, double* c, int64_t nc);
+
 /* --- seeded device inputs ------------------------------------------------ */
 /* Counter-based uniform[-1,1) generator on the device (for operands too large
  * to produce on the host): v = 2u - 1 with u from splitmix64(seed, index). */

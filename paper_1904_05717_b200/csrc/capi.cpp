@@ -672,6 +672,13 @@ int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, 
     });
 }
 
+int tm_fill_seeded(uint64_t seed, double* a, int64_t na, double* b, int64_t nb, double* c, int64_t nc) {
+    return guard([&] {
+        if (!a && na > 0) fail_usage("null A buffer");
+        fill_seeded(seed, a, na, b, nb, c, nc);
+    });
+}
+
 int tm_measure_fp64_peak(int launches, double* tflops) {
     return guard([&] { cuda_check(gpu::measure_fp64_peak(launches < 1 ? 1 : launches, tflops), "fp64 peak probe"); });
 }

@@ -208,4 +208,7 @@ double streaming_flops_per_element(Opnd variant, i64 b1, i64 b2);
 double goto_flops_per_element(i64 k_c, i64 n_c);
 double roofline(double intensity, double peak, double bandwidth);
 
+// Seeded inputs of the reference's `run` command (host/seeded.cpp).
+void fill_seeded(uint64_t seed, double* a, int64_t na, double* b, int64_t nb, double* c, int64_t nc);
+
 }  // namespace mmm

@@ -587,6 +587,20 @@ def execute(nest: LoopNest, A, B, C_, opts: ExecOptions = None, stream=None) -> 
         raise ValueError("operands must be all on the device or all on the host")
 
 
+def fill_seeded(seed: int, shapes):
+    """Host inputs exactly as the reference's `run` command fills them
+    (mt19937_64 uniform(-1,1), operands in order). Returns flat
+    column-major float64 numpy arrays."""
+    import numpy as np
+
+    arrs = [np.empty(r * c, dtype=np.float64) for r, c in shapes] + [None] * (3 - len(shapes))
+    args = []
+    for x in arrs[:3]:
+        args += [x.ctypes.data if x is not None else None, x.size if x is not None else 0]
+    _check(N.lib().tm_fill_seeded(seed, *args))
+    return [x for x in arrs if x is not None]
+
+
 DTYPES = {"bf16": 1, "tf32": 2}
 
 

@@ -1,0 +1,61 @@
+"""The CLI (python -m paper_1904_05717_b200), restating the reference's CLI
+tests (tests/test_cli.cpp:24-68, :105-125) on the CPU-side subcommands;
+`run` needs a GPU and is covered in tests/test_gpu_cli.py."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+I7 = os.path.join(ROOT, "configs", "i7_7700k_like.json")
+
+
+def cli(args):
+    r = subprocess.run([sys.executable, "-m", "paper_1904_05717_b200"] + args, cwd=ROOT, capture_output=True,
+                       text=True, timeout=120)
+    return r.returncode, r.stdout, r.stderr
+
+
+def setup_module(_):
+    # the i7-7700K hierarchy of the reference's configs, in FP64 elements (restated values)
+    os.makedirs(os.path.dirname(I7), exist_ok=True)
+    json.dump({"levels": [{"index": 0, "capacity_elements": 64}, {"index": 1, "capacity_elements": 8192},
+                          {"index": 2, "capacity_elements": 32768}, {"index": 3, "capacity_elements": 786432}]},
+              open(I7, "w"))
+
+
+def test_analyze_published_intensities():
+    rc, out, _ = cli(["analyze", "--alg", "B3A2C0", "--shape", "76800", "--hier", I7, "--bs", "3:n=768", "--bs",
+                      "3:k=768", "--bs", "2:m=120", "--bs", "2:k=192", "--format", "json"])
+    assert rc == 0
+    assert 63.0 < json.loads(out)["intensity_flops_per_byte"] < 64.5
+    rc, out, _ = cli(["analyze", "--alg", "A2C0", "--shape", "192000", "--hier", I7, "--bs", "2:m=120", "--bs",
+                      "2:k=192", "--bs", "3:n=3000", "--format", "json"])
+    assert rc == 0
+    assert 23.1 < json.loads(out)["intensity_flops_per_byte"] < 23.4
+
+
+def test_exit_codes_and_determinism():
+    rc, out, _ = cli(["analyze", "--alg", "B3A2C0", "--shape", "1024", "--hier", "/nonexistent/h.json"])
+    assert rc == 2 and "level" not in out
+    rc, out, err = cli(["analyze", "--alg", "A3A2C0", "--shape", "64", "--hier", I7])
+    assert rc == 1 and "consecutive_resident_equal" in out + err
+    a = cli(["analyze", "--alg", "B3A2C0", "--shape", "4096", "--hier", I7, "--format", "json"])
+    b = cli(["analyze", "--alg", "B3A2C0", "--shape", "4096", "--hier", I7, "--format", "json"])
+    assert a[0] == 0 and a[1] == b[1]
+    c = cli(["analyze", "--alg", "B3A2C0", "--shape", "4096", "--hier", I7, "--format", "csv"])
+    assert c[0] == 0 and c[1].startswith("level,operand,reads,writes\n")
+
+
+def test_plan_on_gpu_hierarchy_file():
+    h = os.path.join(ROOT, "configs", "b200_fp64.json")
+    rc, out, _ = cli(["plan", "--shape", "65536x256x1024", "--hier", h])
+    assert rc == 0
+    j = json.loads(out)
+    # B resident at L2 moves only compulsory traffic for the panel-panel shape
+    assert j["recommended"] == "B2A1C0"
+    assert j["reference_select_algorithm"] == "C"
+    ranked = [r["algorithm"] for r in j["ranking"] if r["model_bytes_into_L2"] is not None]
+    assert ranked[0] == "B2A1C0"
