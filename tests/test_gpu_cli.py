@@ -29,6 +29,9 @@ def test_run_verifies_and_is_deterministic():
     for key in ("algorithm", "shape", "verified", "rel_frobenius_error"):
         assert a[key] == b[key]
     rc, out, _ = run(["--alg", "C2A1C0", "--shape", "2048", "--numerics", "exact", "--format", "json"])
+    assert rc == 0 and json.loads(out)["verified"] is False  # 2048^3 > --verify-max 2^27 (tilemul_main.cpp:265)
+    rc, out, _ = run(["--alg", "C2A1C0", "--shape", "1024", "--numerics", "exact", "--verify-max", str(1 << 31),
+                      "--format", "json"])
     assert rc == 0 and json.loads(out)["rel_frobenius_error"] == 0.0
 
 
