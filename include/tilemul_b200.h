@@ -86,7 +86,8 @@ typedef struct {
     int32_t schedule;   /* TM_SCHEDULE_* */
     int32_t split_k;    /* fused schedule: k splits per tile, deterministic reduction (1 = none, 0 = auto) */
     int32_t ctas;       /* persistent grid size (0 = SMs x occupancy) */
-    int32_t tile;       /* CTA tile rows: 128 or 64 (0 = auto from the register tile) */
+    int32_t tile;       /* CTA tile rows: 128 or 64 (0 = auto from the register tile); tensor-core path:
+                           128 = one SM (cta_group::1), 0/256 = an SM pair (cta_group::2) */
     int32_t tile_n;     /* CTA tile columns (0 = same as tile); 128 x 64 runs two CTAs per SM */
 } tm_exec_opts;
 

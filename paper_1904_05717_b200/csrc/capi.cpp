@@ -195,8 +195,11 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
     auto s = std::make_unique<Schedule>();
     s->kernel = kernel;
     gpu::KernelInfo info{};
+    const bool pair = kernel == gpu::kTc2Bf16 || kernel == gpu::kTc2Tf32;
     if (kernel == gpu::kTcBf16 || kernel == gpu::kTcTf32)
         info = gpu::KernelInfo{128, 256, 256, gpu::tc_smem_bytes(kernel == gpu::kTcTf32), 1};
+    else if (pair)
+        info = gpu::KernelInfo{256, 256, 256, gpu::tc2_smem_bytes(kernel == gpu::kTc2Tf32), 1};
     else
         cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
     const int slots = sm_count() * std::max(1, info.ctas_per_sm);
@@ -224,7 +227,7 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
             const i64 nt = static_cast<i64>(tiles.size());
             if (nt * 2 <= slots) split = static_cast<int>(std::min<i64>(slots / nt, std::max<i64>(1, e.k / 1024)));
         }
-        const i64 slab = (kernel == gpu::kTcBf16 || kernel == gpu::kTcTf32) ? 64 : 32;
+        const i64 slab = (kernel >= gpu::kTcBf16) ? 64 : 32;
         split = std::max(1, std::min<int>(split, static_cast<int>(cdiv(e.k, slab))));
         s->slices = split;
         // k ranges aligned to the kernel's k-slab
@@ -292,6 +295,7 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
     // schedule's waits to make progress.
     int grid = o.ctas > 0 ? std::min(o.ctas, slots) : slots;
     s->grid = std::max(1, std::min<int>(grid, static_cast<int>(T.size())));
+    if (pair) s->grid = 2 * std::max(1, std::min<int>(slots / 2, static_cast<int>(T.size())));  // clusters of 2
     cuda_check(cudaGetDevice(&s->device), "cudaGetDevice");
     cuda_check(cudaMalloc(&s->tasks, sizeof(gpu::Task) * std::max<std::size_t>(1, T.size())), "cudaMalloc(tasks)");
     // Stream-ordered upload, completed before the schedule is used: a plain
@@ -639,7 +643,10 @@ int tm_execute_tc(tm_plan* plan, int dtype, const void* A, int64_t lda, const vo
         if (o.schedule != TM_SCHEDULE_FUSED) fail_usage("tensor-core path runs the fused schedule only");
         if (o.split_k > 1) fail_usage("tensor-core path does not split k");
         o.split_k = 1;
-        const gpu::Kernel kernel = dtype == TM_DTYPE_TF32 ? gpu::kTcTf32 : gpu::kTcBf16;
+        if (o.tile != 0 && o.tile != 128 && o.tile != 256) fail_usage("tensor-core tile must be 128 (1 SM) or 256 (SM pair)");
+        const bool pair = o.tile != 128;
+        const gpu::Kernel kernel = dtype == TM_DTYPE_TF32 ? (pair ? gpu::kTc2Tf32 : gpu::kTcTf32)
+                                                          : (pair ? gpu::kTc2Bf16 : gpu::kTcBf16);
         std::lock_guard<std::mutex> lk(plan->mu);
         Key key{o.schedule, kernel, 1, o.ctas, false};
         auto& slot = plan->schedules[key];
@@ -647,8 +654,11 @@ int tm_execute_tc(tm_plan* plan, int dtype, const void* A, int64_t lda, const vo
         cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
         if (!slot || slot->device != dev) slot = lower(plan->nest, o, kernel, static_cast<cudaStream_t>(stream));
         Schedule& s = *slot;
-        cuda_check(gpu::launch_tc(dtype == TM_DTYPE_TF32, A, lda, B, ldb, C, ldc, e.m, e.n, e.k, s.tasks,
-                                  static_cast<int>(s.host_tasks.size()), s.grid, static_cast<cudaStream_t>(stream)),
+        const int nt = static_cast<int>(s.host_tasks.size());
+        cuda_check(pair ? gpu::launch_tc_pair(dtype == TM_DTYPE_TF32, A, lda, B, ldb, C, ldc, e.m, e.n, e.k, s.tasks,
+                                              nt, s.grid, static_cast<cudaStream_t>(stream))
+                        : gpu::launch_tc(dtype == TM_DTYPE_TF32, A, lda, B, ldb, C, ldc, e.m, e.n, e.k, s.tasks, nt,
+                                         s.grid, static_cast<cudaStream_t>(stream)),
                    "tensor-core kernel launch (TMA needs 16-byte aligned bases and leading dimensions)");
         plan->last_tasks = static_cast<int64_t>(s.host_tasks.size());
         plan->last_launches = 1;

@@ -46,7 +46,9 @@ enum Kernel : int {
     kDmma128x64 = 5,  // 128x64 C tile, 4 warps of 64x32, two CTAs per SM (prologue/epilogue overlap)
     kKernelCount = 6,
     kTcBf16 = 100,    // tcgen05 BF16 inputs, fp32 TMEM accumulate, 128x256 tile (tc_gemm_sm100.cu)
-    kTcTf32 = 101     // tcgen05 TF32 inputs
+    kTcTf32 = 101,    // tcgen05 TF32 inputs
+    kTc2Bf16 = 102,   // tcgen05.mma.cta_group::2: 2-CTA cluster, 256x256 tile per pair
+    kTc2Tf32 = 103
 };
 
 struct KernelInfo {
@@ -71,6 +73,11 @@ cudaError_t launch_tc(bool tf32, const void* A, int64_t lda, const void* B, int6
 // fp64 -> bf16 (RNE) or fp64 -> tf32-valued fp32 (RNE to 11 significant bits).
 cudaError_t launch_round(bool tf32, const double* x, void* y, int64_t count, cudaStream_t stream);
 int tc_smem_bytes(bool tf32);
+// Same contract, 2-SM pair kernel: tasks are 256 x 256 tiles, grid even (clusters of 2).
+cudaError_t launch_tc_pair(bool tf32, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
+                           int64_t m, int64_t n, int64_t k, const Task* tasks, int ntasks, int grid,
+                           cudaStream_t stream);
+int tc2_smem_bytes(bool tf32);
 cudaError_t launch_fill_block(double* x, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
                               int64_t col0, int64_t gld, cudaStream_t stream);
 cudaError_t launch_fill(double* x, int64_t count, uint64_t seed, uint64_t offset, cudaStream_t stream);

@@ -111,6 +111,23 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])   \
         : "r"(taddr))
 
+// C(row, c0 .. c0+31) += acc for one thread's row: all 32 loads are issued
+// before any add (a dependent load/add/store per column would serialise
+// ~32 memory latencies per chunk and make the epilogue, not the MMA, the
+// critical path). Consecutive lanes own consecutive rows, so every column
+// access of a warp is one coalesced 128-byte line.
+__device__ __forceinline__ void epilogue_chunk(float* c, int64_t ldc, int ncols, const uint32_t (&r)[32]) {
+    if (ncols >= 32) {
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __ldcs(c + j * ldc);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) __stcs(c + j * ldc, v[j] + __uint_as_float(r[j]));
+    } else {
+        for (int j = 0; j < ncols; ++j) c[j * ldc] = c[j * ldc] + __uint_as_float(r[j]);
+    }
+}
+
 struct TcArgs {
     float* C;
     int64_t ldc;
@@ -255,16 +272,7 @@ __global__ void __launch_bounds__(256, 1) k_tc(const __grid_constant__ CUtensorM
                                        static_cast<uint32_t>(acc * kTcBN + cb * 32);
                 TC_LD32(taddr, r);
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                if (live) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int col = cb * 32 + j;
-                        if (col < t.n) {
-                            float* p = crow + static_cast<int64_t>(col) * a.ldc;
-                            *p = *p + __uint_as_float(r[j]);
-                        }
-                    }
-                }
+                if (live) epilogue_chunk(crow + static_cast<int64_t>(cb * 32) * a.ldc, a.ldc, t.n - cb * 32, r);
             }
             tc_fence_before();
             __syncwarp();
@@ -280,6 +288,234 @@ __global__ void __launch_bounds__(256, 1) k_tc(const __grid_constant__ CUtensorM
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
+    }
+}
+
+// ======================= 2-SM pair kernel (cta_group::2) =======================
+// A cluster of two CTAs on one TPC computes a 256 x 256 C tile with
+// tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and
+// its 128 columns of B (so each SM ingests 32 KB per 64-deep bf16 stage for a
+// 128 x 256 result, two thirds of the single-CTA kernel's 48 KB), the leader
+// (rank 0) issues the MMAs, each CTA's TMEM holds its own 128 accumulator
+// rows. Barrier protocol (the one CUTLASS's 2-SM pipelines use):
+//   full[s]   leader only; armed by the leader's producer with both CTAs'
+//             bytes; both CTAs' 2-SM TMA loads complete_tx on it;
+//   empty[s]  both CTAs; the leader's MMA commit multicasts to both;
+//   tfull[a]  both CTAs; the leader's per-tile commit multicasts to both;
+//   tempty[a] leader only; the 4 epilogue warps of both CTAs arrive (count 8).
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(const void* p, uint32_t rank) {
+    uint32_t out;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(out) : "r"(saddr(p)), "r"(rank));
+    return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];\n" ::"r"(saddr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+template <bool TF32>
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+    if constexpr (TF32) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            saddr(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
+template <bool TF32>
+struct Tc2Geo {
+    static constexpr int E = TF32 ? 4 : 2;
+    static constexpr int BK = 128 / E;
+    static constexpr int MATOM = 128 / E;
+    static constexpr int A_BOXES = 128 / MATOM;  // this CTA's 128 rows
+    static constexpr int A_BOX_BYTES = 128 * BK;
+    static constexpr int A_BYTES = 128 * BK * E;
+    static constexpr int B_BYTES = 128 * BK * E;  // this CTA's 128 columns
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int PAIR_STAGE_BYTES = 2 * STAGE;
+    static constexpr int UK = 32 / E;
+    static constexpr int NMMA = BK / UK;
+    static constexpr int STAGES = 6;
+    static constexpr uint32_t A_LAYOUT = TF32 ? 1u : 2u;
+    static constexpr uint32_t A_SBO = TF32 ? 512u : 1024u;
+    static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+
+template <bool TF32>
+__host__ __device__ constexpr uint32_t instr_desc_pair() {
+    return (1u << 4) | ((TF32 ? 2u : 1u) << 7) | ((TF32 ? 2u : 1u) << 10) | (1u << 15) | (0u << 16) |
+           (static_cast<uint32_t>(256 >> 3) << 17) | (static_cast<uint32_t>(256 >> 4) << 24);
+}
+
+template <bool TF32>
+__global__ void __launch_bounds__(256, 1) k_tc2(const __grid_constant__ CUtensorMap tmA,
+                                                const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+    using G = Tc2Geo<TF32>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::STAGES * G::STAGE);
+    uint64_t* empty = full + G::STAGES;
+    uint64_t* tfull = empty + G::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < G::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&tfull[s], 1);
+            mbar_init(&tempty[s], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(saddr(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();  // barriers of both CTAs initialised and TMEM allocated before any remote traffic
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int ti = cluster; ti < a.ntasks; ti += nclusters) {
+                const Task t = a.tasks[ti];
+                const int nk = (t.k + G::BK - 1) / G::BK;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * G::STAGE;
+                    uint8_t* sb = sa + G::A_BYTES;
+                    if (leader) mbar_expect_tx(&full[stage], G::PAIR_STAGE_BYTES);
+                    const uint32_t bar = mapa_rank(&full[stage], 0);
+                    const int kc = t.p0 + kb * G::BK;
+#pragma unroll
+                    for (int h = 0; h < G::A_BOXES; ++h)
+                        tma_load_2d_pair(sa + h * G::A_BOX_BYTES, &tmA, bar,
+                                         t.i0 + static_cast<int>(rank) * 128 + h * G::MATOM, kc);
+                    tma_load_2d_pair(sb, &tmB, bar, kc, t.j0 + static_cast<int>(rank) * 128);
+                    if (++stage == G::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only)
+            constexpr uint32_t idesc = instr_desc_pair<TF32>();
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t aphase = 0;
+            for (int ti = cluster; ti < a.ntasks; ti += nclusters) {
+                const Task t = a.tasks[ti];
+                const int nk = (t.k + G::BK - 1) / G::BK;
+                mbar_wait(&tempty[acc], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + static_cast<uint32_t>(acc * 256);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = saddr(smem + stage * G::STAGE);
+                    const uint32_t sb = sa + G::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < G::NMMA; ++kk) {
+                        const uint64_t da = smem_desc(sa + kk * G::UK * 128, G::A_BOX_BYTES, G::A_SBO, G::A_LAYOUT);
+                        const uint64_t db = smem_desc(sb + kk * 32, 16, 1024);
+                        umma_pair<TF32>(tmem_d, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+                    }
+                    umma_commit_pair(&empty[stage]);
+                    if (++stage == G::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit_pair(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    aphase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue (both CTAs, own 128 rows)
+        const int ew = warp - 4;
+        const int row = static_cast<int>(rank) * 128 + ew * 32 + lane;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int ti = cluster; ti < a.ntasks; ti += nclusters) {
+            const Task t = a.tasks[ti];
+            mbar_wait(&tfull[acc], aphase);
+            tc_fence_after();
+            const bool live = row < t.m;
+            float* crow = a.C + (static_cast<int64_t>(t.i0) + row) + static_cast<int64_t>(t.j0) * a.ldc;
+#pragma unroll 1
+            for (int cb = 0; cb < 256 / 32; ++cb) {
+                uint32_t r[32];
+                const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) +
+                                       static_cast<uint32_t>(acc * 256 + cb * 32);
+                TC_LD32(taddr, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                if (live) epilogue_chunk(crow + static_cast<int64_t>(cb * 32) * a.ldc, a.ldc, t.n - cb * 32, r);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(mapa_rank(&tempty[acc], 0));
+            if (++acc == 2) {
+                acc = 0;
+                aphase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // no CTA leaves (or frees TMEM) while its peer may still signal it
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
     }
 }
 
@@ -357,7 +593,54 @@ __global__ void k_round_tf32(const double* x, float* y, int64_t count) {
     }
 }
 
+template <bool TF32>
+cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc, int64_t m,
+                         int64_t n, int64_t k, const Task* tasks, int ntasks, int grid, cudaStream_t stream) {
+    using G = Tc2Geo<TF32>;
+    cudaError_t e = encoder();
+    if (e != cudaSuccess) return e;
+    if ((lda * G::E) % 16 || (ldb * G::E) % 16 || reinterpret_cast<uintptr_t>(A) % 16 ||
+        reinterpret_cast<uintptr_t>(B) % 16)
+        return cudaErrorInvalidValue;
+    CUtensorMap ma, mb;
+    if ((e = make_map(&ma, A, TF32, m, k, lda, G::MATOM, G::BK,
+                      TF32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess)
+        return e;
+    if ((e = make_map(&mb, B, TF32, k, n, ldb, G::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
+    static bool attr[2] = {false, false};
+    if (!attr[TF32]) {
+        if ((e = cudaFuncSetAttribute(k_tc2<TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM)) !=
+            cudaSuccess)
+            return e;
+        attr[TF32] = true;
+    }
+    TcArgs args{C, ldc, tasks, ntasks};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_tc2<TF32>, ma, mb, args);
+}
+
 }  // namespace
+
+cudaError_t launch_tc_pair(bool tf32, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
+                           int64_t m, int64_t n, int64_t k, const Task* tasks, int ntasks, int grid,
+                           cudaStream_t stream) {
+    if (ntasks <= 0) return cudaSuccess;
+    return tf32 ? launch_tc2_t<true>(A, lda, B, ldb, C, ldc, m, n, k, tasks, ntasks, grid, stream)
+                : launch_tc2_t<false>(A, lda, B, ldb, C, ldc, m, n, k, tasks, ntasks, grid, stream);
+}
+
+int tc2_smem_bytes(bool tf32) { return tf32 ? Tc2Geo<true>::SMEM : Tc2Geo<false>::SMEM; }
 
 cudaError_t launch_tc(bool tf32, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                       int64_t m, int64_t n, int64_t k, const Task* tasks, int ntasks, int grid, cudaStream_t stream) {

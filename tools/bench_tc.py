@@ -26,37 +26,47 @@ def main():
     m = n = k = size
     hier = T.CacheHierarchy.from_capacities([128 * 512, 232448 // 2, 132644864 // 2])
     d = T.parse_name("C2A1C0")
-    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(128, 256)),
-                             pinned=T.BlocksizeSet({(1, "m"): 128, (2, "m"): 1536, (2, "n"): 3072}))
-    nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+    def plan(tile):
+        bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(tile, 256)),
+                                 pinned=T.BlocksizeSet({(1, "m"): tile, (2, "m"): 1536, (2, "n"): 3072}))
+        return T.build_plan(d, bs, hier, T.Shape(m, n, k)), bs
+
     A64 = torch.empty(m * k, dtype=torch.float64, device="cuda")
     B64 = torch.empty(k * n, dtype=torch.float64, device="cuda")
     T.fill_uniform_device(A64, 1)
     T.fill_uniform_device(B64, 2)
-    for dtype in ("bf16", "tf32"):
+    for dtype, tile in (("bf16", 256), ("bf16", 128), ("tf32", 256), ("tf32", 128)):
+        nest, bs = plan(tile)
         A = T.round_inputs(A64, dtype)
         B = T.round_inputs(B64, dtype)
         C = torch.zeros(m * n, dtype=torch.float32, device="cuda")
         for _ in range(2):
-            T.execute_tc(nest, A, B, C, dtype)
+            T.execute_tc(nest, A, B, C, dtype, T.ExecOptions(tile=tile))
         torch.cuda.synchronize()
         ts = []
-        for _ in range(5):
+        import bench
+        clk = bench.ClockSampler(0)
+        clk.__enter__()
+        for _ in range(40):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            T.execute_tc(nest, A, B, C, dtype)
+            T.execute_tc(nest, A, B, C, dtype, T.ExecOptions(tile=tile))
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e-3)
+        clk.__exit__(None, None, None)
         t = statistics.median(ts)
         tf = 2.0 * m * n * k / t / 1e12
         peak = peaks["bf16_tflops"] if dtype == "bf16" else peaks["bf16_tflops"] / 2
         print(json.dumps({"config": "config4", "dtype": dtype, "shape": [m, n, k], "seconds": t, "tflops": tf,
                           "peak_tflops": peak,
                           "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" + (" / 2 (nominal tf32:bf16 dense ratio)" if dtype == "tf32" else ""),
-                          "frac": tf / peak, "cta_tile": "128x256 (cta_group::1)",
+                          "frac": tf / peak,
+                          "frac_of_sustained": tf / (peaks.get("bf16_tflops_sustained", peak * 2) /
+                                                    (1 if dtype == "bf16" else 2)),
+                          "cta_tile": "256x256 per SM pair (cta_group::2)" if tile == 256 else "128x256 (cta_group::1)",
                           "blocksizes": {f"{lv}:{dd}": v for (lv, dd), v in bs.entries()},
-                          "launch": nest.last_launch()}), flush=True)
+                          "launch": nest.last_launch(), "clocks": clk.summary()}), flush=True)
         del A, B, C
 
 
