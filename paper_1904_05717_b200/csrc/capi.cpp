@@ -133,11 +133,11 @@ struct tm_plan {
     std::mutex mu;
     // host-buffer execution
     double *dA = nullptr, *dB = nullptr, *dC = nullptr;
-    cudaStream_t host_stream = nullptr, copy_stream = nullptr;
+    cudaStream_t host_stream = nullptr, copy_stream = nullptr, d2h_stream = nullptr;
     std::vector<cudaEvent_t> chunk_ready;
-    // k-chunk sub-plans of the host-buffer pipeline (same family and
-    // blocksizes, k extent = one chunk / the tail chunk)
-    std::unique_ptr<tm_plan> chunk_full, chunk_tail;
+    // sub-plans of the host-buffer pipeline, keyed by (n, k) extent of one
+    // (column block, k-chunk) piece: same family and blocksizes
+    std::map<std::pair<int64_t, int64_t>, std::unique_ptr<tm_plan>> chunk_plans;
     int64_t last_tasks = 0;
     int32_t last_launches = 0, last_ctas = 0;
     ~tm_plan() {
@@ -147,6 +147,7 @@ struct tm_plan {
         for (auto ev : chunk_ready) cudaEventDestroy(ev);
         if (host_stream) cudaStreamDestroy(host_stream);
         if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (d2h_stream) cudaStreamDestroy(d2h_stream);
     }
 };
 
@@ -552,8 +553,10 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
         const Extents& e = plan->nest.ext;
         const std::size_t na = static_cast<std::size_t>(e.m * e.k), nb = static_cast<std::size_t>(e.k * e.n),
                           nc = static_cast<std::size_t>(e.m * e.n);
-        if (!plan->host_stream)
-            cuda_check(cudaStreamCreateWithFlags(&plan->host_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        auto mkstream = [](cudaStream_t& s) {
+            if (!s) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+        };
+        mkstream(plan->host_stream);
         if (!plan->dA) {
             cuda_check(cudaMalloc(&plan->dA, na * sizeof(double)), "cudaMalloc(A)");
             cuda_check(cudaMalloc(&plan->dB, nb * sizeof(double)), "cudaMalloc(B)");
@@ -562,71 +565,102 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
         cudaStream_t st = plan->host_stream;
         tm_exec_opts o{};
         if (opts) o = *opts;
-        // Pipeline: C first, then A and B in k-chunks on a copy stream, each
-        // chunk's GEMM on the compute stream as soon as its operands landed.
-        // Chunks are multiples of the 32-deep slab and run in ascending k, so
-        // every C entry sees exactly the unchunked operation sequence.
-        const int nchunks = (o.schedule == TM_SCHEDULE_FUSED && o.split_k <= 1 && e.k >= 4096)
-                                ? static_cast<int>(std::min<i64>(8, e.k / 2048))
-                                : 1;
-        if (nchunks == 1) {
+        const bool pipelined = o.schedule == TM_SCHEDULE_FUSED && o.split_k <= 1 && (e.k >= 4096 || e.n >= 4096);
+        if (!pipelined) {
             cuda_check(cudaMemcpyAsync(plan->dA, A, na * sizeof(double), cudaMemcpyHostToDevice, st), "H2D A");
             cuda_check(cudaMemcpyAsync(plan->dB, B, nb * sizeof(double), cudaMemcpyHostToDevice, st), "H2D B");
             cuda_check(cudaMemcpyAsync(plan->dC, C, nc * sizeof(double), cudaMemcpyHostToDevice, st), "H2D C");
             run(plan, plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, opts, st);
-        } else {
-            const i64 kc = cdiv(cdiv(e.k, nchunks), 32) * 32;
-            const int nq = static_cast<int>(cdiv(e.k, kc));
-            const i64 ktail = e.k - (nq - 1) * kc;
-            auto sub = [&](std::unique_ptr<tm_plan>& slot, i64 kk) -> tm_plan* {
-                if (!slot || slot->nest.ext.k != kk) {
-                    slot = std::make_unique<tm_plan>();
-                    slot->nest = plan->nest;
-                    slot->nest.ext.k = kk;
-                    slot->hier = plan->hier;
+            cuda_check(cudaMemcpyAsync(C, plan->dC, nc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H C");
+            cuda_check(cudaStreamSynchronize(st), "execute_host sync");
+            return;
+        }
+        // Two-level copy/compute pipeline: C column blocks outer, k-chunks
+        // inner. Block b's C goes up just ahead of its GEMMs and comes back on
+        // a third stream while block b+1 computes; A streams in k-chunks
+        // during block 0, B in (k-chunk, column-block) pieces. Every C entry
+        // still sees its k chunks in ascending order (chunks are multiples of
+        // the 32-deep slab), i.e. exactly the unpipelined operation sequence.
+        mkstream(plan->copy_stream);
+        mkstream(plan->d2h_stream);
+        const int nq0 = e.k >= 4096 ? static_cast<int>(std::min<i64>(8, e.k / 2048)) : 1;
+        const i64 kc = cdiv(cdiv(e.k, nq0), 32) * 32;
+        const int nq = static_cast<int>(cdiv(e.k, kc));
+        const int nb0 = e.n >= 2048 ? static_cast<int>(std::min<i64>(8, e.n / 1024)) : 1;
+        const i64 wb = cdiv(cdiv(e.n, nb0), 128) * 128;
+        const int nbk = static_cast<int>(cdiv(e.n, wb));
+        const std::size_t nev = static_cast<std::size_t>(nq + 2 * nbk + nbk * nq);
+        while (plan->chunk_ready.size() < nev) {
+            cudaEvent_t ev;
+            cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+            plan->chunk_ready.push_back(ev);
+        }
+        cudaEvent_t* evA = plan->chunk_ready.data();
+        cudaEvent_t* evC = evA + nq;
+        cudaEvent_t* evDone = evC + nbk;
+        cudaEvent_t* evB = evDone + nbk;
+        auto sub = [&](i64 nn, i64 kk) -> tm_plan* {
+            auto& slot = plan->chunk_plans[{nn, kk}];
+            if (!slot) {
+                slot = std::make_unique<tm_plan>();
+                slot->nest = plan->nest;
+                slot->nest.ext.n = nn;
+                slot->nest.ext.k = kk;
+                slot->hier = plan->hier;
+            }
+            return slot.get();
+        };
+        cudaStream_t cs = plan->copy_stream, ds = plan->d2h_stream;
+        const std::size_t ld = static_cast<std::size_t>(e.k) * sizeof(double);
+        int64_t tasks = 0;
+        int32_t launches = 0, ctas = 0;
+        auto d2h = [&](int b) {
+            const i64 j0 = b * wb, w = std::min(wb, e.n - j0);
+            cuda_check(cudaStreamWaitEvent(ds, evDone[b], 0), "wait block");
+            cuda_check(cudaMemcpyAsync(C + j0 * e.m, plan->dC + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
+                                       cudaMemcpyDeviceToHost, ds),
+                       "D2H C block");
+        };
+        for (int b = 0; b < nbk; ++b) {
+            const i64 j0 = b * wb, w = std::min(wb, e.n - j0);
+            cuda_check(cudaMemcpyAsync(plan->dC + j0 * e.m, C + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
+                                       cudaMemcpyHostToDevice, cs),
+                       "H2D C block");
+            cuda_check(cudaEventRecord(evC[b], cs), "event");
+            for (int q = 0; q < nq; ++q) {
+                const i64 p0 = q * kc, kq = std::min(kc, e.k - p0);
+                if (b == 0) {
+                    cuda_check(cudaMemcpyAsync(plan->dA + p0 * e.m, A + p0 * e.m,
+                                               static_cast<std::size_t>(kq * e.m) * 8, cudaMemcpyHostToDevice, cs),
+                               "H2D A chunk");
+                    cuda_check(cudaEventRecord(evA[q], cs), "event");
                 }
-                return slot.get();
-            };
-            tm_plan* pf = sub(plan->chunk_full, kc);
-            tm_plan* pt = ktail == kc ? pf : sub(plan->chunk_tail, ktail);
-            if (!plan->copy_stream)
-                cuda_check(cudaStreamCreateWithFlags(&plan->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
-            while (static_cast<int>(plan->chunk_ready.size()) < nq) {
-                cudaEvent_t ev;
-                cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
-                plan->chunk_ready.push_back(ev);
-            }
-            cudaStream_t cs = plan->copy_stream;
-            cuda_check(cudaMemcpyAsync(plan->dC, C, nc * sizeof(double), cudaMemcpyHostToDevice, cs), "H2D C");
-            for (int q = 0; q < nq; ++q) {
-                const i64 p0 = q * kc, kq = q + 1 == nq ? ktail : kc;
-                cuda_check(cudaMemcpyAsync(plan->dA + p0 * e.m, A + p0 * e.m,
-                                           static_cast<std::size_t>(kq * e.m) * sizeof(double),
-                                           cudaMemcpyHostToDevice, cs),
-                           "H2D A chunk");
-                cuda_check(cudaMemcpy2DAsync(plan->dB + p0, static_cast<std::size_t>(e.k) * sizeof(double), B + p0,
-                                             static_cast<std::size_t>(e.k) * sizeof(double),
-                                             static_cast<std::size_t>(kq) * sizeof(double),
-                                             static_cast<std::size_t>(e.n), cudaMemcpyHostToDevice, cs),
-                           "H2D B chunk");
-                cuda_check(cudaEventRecord(plan->chunk_ready[static_cast<std::size_t>(q)], cs), "event record");
-            }
-            int64_t tasks = 0;
-            int32_t launches = 0;
-            for (int q = 0; q < nq; ++q) {
-                const i64 p0 = q * kc;
-                cuda_check(cudaStreamWaitEvent(st, plan->chunk_ready[static_cast<std::size_t>(q)], 0), "wait chunk");
-                tm_plan* pq = q + 1 == nq ? pt : pf;
-                run(pq, plan->dA + p0 * e.m, e.m, plan->dB + p0, e.k, plan->dC, e.m, &o, st);
+                cuda_check(cudaMemcpy2DAsync(plan->dB + p0 + j0 * e.k, ld, B + p0 + j0 * e.k, ld,
+                                             static_cast<std::size_t>(kq) * 8, static_cast<std::size_t>(w),
+                                             cudaMemcpyHostToDevice, cs),
+                           "H2D B piece");
+                cudaEvent_t eb = evB[b * nq + q];
+                cuda_check(cudaEventRecord(eb, cs), "event");
+                // issue the GEMM right away so pageable-memory copies (which
+                // block the host while staging) still overlap device compute
+                if (q == 0) cuda_check(cudaStreamWaitEvent(st, evC[b], 0), "wait C block");
+                cuda_check(cudaStreamWaitEvent(st, evA[q], 0), "wait A chunk");
+                cuda_check(cudaStreamWaitEvent(st, eb, 0), "wait B piece");
+                tm_plan* pq = sub(w, kq);
+                run(pq, plan->dA + p0 * e.m, e.m, plan->dB + p0 + j0 * e.k, e.k, plan->dC + j0 * e.m, e.m, &o, st);
                 tasks += pq->last_tasks;
                 launches += pq->last_launches;
+                ctas = pq->last_ctas;
             }
-            plan->last_tasks = tasks;
-            plan->last_launches = launches;
-            plan->last_ctas = pf->last_ctas;
+            cuda_check(cudaEventRecord(evDone[b], st), "event");
+            if (b > 0) d2h(b - 1);  // one block behind: a pageable D2H blocks the host until it lands
         }
-        cuda_check(cudaMemcpyAsync(C, plan->dC, nc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H C");
+        d2h(nbk - 1);
+        cuda_check(cudaStreamSynchronize(ds), "execute_host sync");
         cuda_check(cudaStreamSynchronize(st), "execute_host sync");
+        plan->last_tasks = tasks;
+        plan->last_launches = launches;
+        plan->last_ctas = ctas;
     });
 }
 
