@@ -84,7 +84,9 @@ enum {
 typedef struct {
     int32_t numerics;   /* TM_NUMERICS_* */
     int32_t schedule;   /* TM_SCHEDULE_* */
-    int32_t split_k;    /* fused schedule: k splits per tile, deterministic reduction (1 = none, 0 = auto) */
+    int32_t split_k;    /* fused schedule: k parts per tile, deterministic reduction. 1 = none; n > 1 = every
+                           tile; 0 = auto (DMMA numerics only): all tiles when C is too small to fill the
+                           GPU, else only the tiles of the last partial wave */
     int32_t ctas;       /* persistent grid size (0 = SMs x occupancy) */
     int32_t tile;       /* CTA tile rows: 128 or 64 (0 = auto from the register tile); tensor-core path:
                            128 = one SM (cta_group::1), 0/256 = an SM pair (cta_group::2) */

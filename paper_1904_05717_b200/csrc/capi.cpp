@@ -101,7 +101,11 @@ struct Schedule {
     gpu::Kernel kernel = gpu::kDmma128;
     bool vec16 = false;
     int grid = 1;
-    int slices = 1;          // split-k slices (fused)
+    int slices = 0;          // number of k-split tiles to reduce (fused)
+    gpu::ReduceTile* reduce = nullptr;
+    int32_t* cta_first = nullptr;  // stream-K: per-CTA task ranges
+    bool blocked = false;
+    int grid_fixed = 0;
     int regions = 0;         // progress counters (faithful)
     std::vector<gpu::Task> host_tasks;
     gpu::Task* tasks = nullptr;
@@ -113,6 +117,8 @@ struct Schedule {
         if (tasks) cudaFree(tasks);
         if (progress) cudaFree(progress);
         if (work) cudaFree(work);
+        if (reduce) cudaFree(reduce);
+        if (cta_first) cudaFree(cta_first);
     }
 };
 
@@ -222,46 +228,161 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
             for_each_subtile(c.i0, c.m, c.j0, c.n, info.tile_m, info.tile_n,
                              [&](i64 i0, i64 m, i64 j0, i64 n) { tiles.push_back({i0, m, j0, n}); });
         });
-        int split = o.split_k;
-        if (split == 0) {  // auto: fill the machine when C has too few tiles
-            split = 1;
-            const i64 nt = static_cast<i64>(tiles.size());
-            if (nt * 2 <= slots) split = static_cast<int>(std::min<i64>(slots / nt, std::max<i64>(1, e.k / 1024)));
-        }
+        const bool dmma = o.numerics == TM_NUMERICS_DMMA && kernel < gpu::kTcBf16;
+        const i64 ntiles = static_cast<i64>(tiles.size());
+        // Stream-K (split_k == -1, or auto when C fills only a few waves with
+        // a ragged last one): every CTA gets an equal contiguous range of
+        // (tile, 32-deep k-slab) iterations; a tile cut by a range boundary
+        // becomes several k-parts reduced in fixed slot order afterwards.
+        // Balances the machine exactly and staggers the tile boundaries
+        // (C loads/stores) of different CTAs in time.
+        const bool ragged = ntiles % slots != 0 && ntiles < 8 * slots && ntiles * 2 > slots;
+        if (dmma && (o.split_k == -1 || (o.split_k == 0 && ragged && e.k >= 2048))) {
+            const i64 slab = 32, nks = cdiv(e.k, slab), U = ntiles * nks;
+            const int G = static_cast<int>(std::min<i64>(slots, U));
+            std::vector<std::vector<std::array<i64, 2>>> pieces(tiles.size());  // per tile: (slab_lo, slab_hi)
+            std::vector<std::vector<std::pair<i64, i64>>> per_cta(static_cast<std::size_t>(G));  // (tile, piece#)
+            for (int c = 0; c < G; ++c) {
+                const i64 lo = U * c / G, hi = U * (c + 1) / G;
+                for (i64 u = lo; u < hi;) {
+                    const i64 tile = u / nks, end = std::min(hi, (tile + 1) * nks);
+                    auto& pc = pieces[static_cast<std::size_t>(tile)];
+                    per_cta[static_cast<std::size_t>(c)].push_back({tile, static_cast<i64>(pc.size())});
+                    pc.push_back({u - tile * nks, end - tile * nks});
+                    u = end;
+                }
+            }
+            std::vector<int32_t> slot0(tiles.size(), -1);
+            std::vector<gpu::ReduceTile> red;
+            int32_t next_slot = 0;
+            for (std::size_t t = 0; t < tiles.size(); ++t)
+                if (pieces[t].size() > 1) {
+                    slot0[t] = next_slot;
+                    red.push_back(gpu::ReduceTile{static_cast<int32_t>(tiles[t][0]), static_cast<int32_t>(tiles[t][2]),
+                                                  static_cast<int32_t>(tiles[t][1]), static_cast<int32_t>(tiles[t][3]),
+                                                  next_slot, static_cast<int32_t>(pieces[t].size())});
+                    next_slot += static_cast<int32_t>(pieces[t].size());
+                }
+            std::vector<int32_t> first(static_cast<std::size_t>(G) + 1, 0);
+            for (int c = 0; c < G; ++c) {
+                first[static_cast<std::size_t>(c)] = static_cast<int32_t>(T.size());
+                for (auto [tile, pi] : per_cta[static_cast<std::size_t>(c)]) {
+                    const auto& t = tiles[static_cast<std::size_t>(tile)];
+                    const auto& pr = pieces[static_cast<std::size_t>(tile)][static_cast<std::size_t>(pi)];
+                    gpu::Task tk{};
+                    tk.i0 = static_cast<int32_t>(t[0]);
+                    tk.m = static_cast<int32_t>(t[1]);
+                    tk.j0 = static_cast<int32_t>(t[2]);
+                    tk.n = static_cast<int32_t>(t[3]);
+                    tk.p0 = static_cast<int32_t>(pr[0] * slab);
+                    tk.k = static_cast<int32_t>(std::min(pr[1] * slab, e.k) - pr[0] * slab);
+                    tk.tile = -1;
+                    tk.seq = 0;
+                    const int32_t s0 = slot0[static_cast<std::size_t>(tile)];
+                    tk.slice = s0 < 0 ? -1 : s0 + static_cast<int32_t>(pi);
+                    tk.from_c = pr[0] == 0 ? 1 : 0;
+                    T.push_back(tk);
+                }
+            }
+            first[static_cast<std::size_t>(G)] = static_cast<int32_t>(T.size());
+            s->slices = static_cast<int>(red.size());
+            s->blocked = true;
+            s->grid_fixed = G;
+            cuda_check(cudaMalloc(&s->cta_first, sizeof(int32_t) * first.size()), "cudaMalloc(cta ranges)");
+            cuda_check(cudaMemcpyAsync(s->cta_first, first.data(), sizeof(int32_t) * first.size(),
+                                       cudaMemcpyHostToDevice, stream),
+                       "upload cta ranges");
+            if (!red.empty()) {
+                s->work_ld = info.tile_m;
+                s->work_slice = static_cast<i64>(info.tile_m) * info.tile_n;
+                cuda_check(cudaMalloc(&s->work, sizeof(double) * static_cast<std::size_t>(s->work_slice) * next_slot),
+                           "cudaMalloc(stream-k workspace)");
+                cuda_check(cudaMalloc(&s->reduce, sizeof(gpu::ReduceTile) * red.size()), "cudaMalloc(reduce list)");
+                cuda_check(cudaMemcpyAsync(s->reduce, red.data(), sizeof(gpu::ReduceTile) * red.size(),
+                                           cudaMemcpyHostToDevice, stream),
+                           "upload reduce list");
+            }
+            cuda_check(cudaStreamSynchronize(stream), "upload stream-k lists (sync)");
+        } else {
+        // k parts per tile. split_k > 1: every tile; split_k == 0 (auto):
+        // every tile when C has too few tiles to fill the machine, otherwise
+        // only the tiles of the last, partial wave (a "tail split": the full
+        // waves run unsplit, the tail's parts fill the idle SMs).
         const i64 slab = (kernel >= gpu::kTcBf16) ? 64 : 32;
-        split = std::max(1, std::min<int>(split, static_cast<int>(cdiv(e.k, slab))));
-        s->slices = split;
-        // k ranges aligned to the kernel's k-slab
-        const i64 per = cdiv(cdiv(e.k, split), slab) * slab;
-        for (const auto& t : tiles)
-            for (int q = 0; q < split; ++q) {
+        const i64 nt = static_cast<i64>(tiles.size());
+        const i64 max_parts = std::max<i64>(1, std::min<i64>(8, e.k / (16 * slab)));
+        std::vector<int> parts(tiles.size(), 1);
+        if (o.split_k > 1) {
+            std::fill(parts.begin(), parts.end(), static_cast<int>(std::min<i64>(o.split_k, cdiv(e.k, slab))));
+        } else if (o.split_k == 0 && nt > 0 && o.numerics == TM_NUMERICS_DMMA) {
+            // (auto-splitting changes the summation order, so it is only
+            // applied where results are bound-checked, never for the
+            // bit-reproducible fma/exact numerics)
+            if (nt * 2 <= slots) {
+                const int sp = static_cast<int>(std::min<i64>(slots / nt, std::max<i64>(1, e.k / 1024)));
+                std::fill(parts.begin(), parts.end(), std::max(1, std::min<int>(sp, static_cast<int>(cdiv(e.k, slab)))));
+            } else {
+                const i64 full = (nt / slots) * slots, rem = nt - full;
+                // tail time in tile units: ceil(rem*S/slots)/S, plus a small
+                // charge per extra part for its partial store and reduction
+                double best = 1.0;
+                int bestS = 1;
+                for (i64 S = 2; S <= max_parts && rem > 0; ++S) {
+                    const double cost = static_cast<double>(cdiv(rem * S, slots)) / static_cast<double>(S) +
+                                        0.03 * static_cast<double>(S - 1);
+                    if (cost < best - 1e-9) {
+                        best = cost;
+                        bestS = static_cast<int>(S);
+                    }
+                }
+                for (i64 i = full; i < nt; ++i) parts[static_cast<std::size_t>(i)] = bestS;
+            }
+        }
+        int32_t next_slot = 0;
+        std::vector<gpu::ReduceTile> red;
+        for (std::size_t ti = 0; ti < tiles.size(); ++ti) {
+            const auto& t = tiles[ti];
+            const i64 per = cdiv(cdiv(e.k, parts[ti]), slab) * slab;
+            const int used = static_cast<int>(cdiv(e.k, per));
+            gpu::Task tk{};
+            tk.i0 = static_cast<int32_t>(t[0]);
+            tk.m = static_cast<int32_t>(t[1]);
+            tk.j0 = static_cast<int32_t>(t[2]);
+            tk.n = static_cast<int32_t>(t[3]);
+            tk.tile = -1;
+            tk.seq = 0;
+            if (used == 1) {
+                tk.p0 = 0;
+                tk.k = static_cast<int32_t>(e.k);
+                tk.slice = -1;
+                tk.from_c = 1;
+                T.push_back(tk);
+                continue;
+            }
+            red.push_back(gpu::ReduceTile{tk.i0, tk.j0, tk.m, tk.n, next_slot, used});
+            for (int q = 0; q < used; ++q) {
                 const i64 p0 = q * per;
-                if (p0 >= e.k) break;
-                gpu::Task tk{};
-                tk.i0 = static_cast<int32_t>(t[0]);
-                tk.m = static_cast<int32_t>(t[1]);
-                tk.j0 = static_cast<int32_t>(t[2]);
-                tk.n = static_cast<int32_t>(t[3]);
                 tk.p0 = static_cast<int32_t>(p0);
                 tk.k = static_cast<int32_t>(std::min(per, e.k - p0));
-                tk.tile = -1;
-                tk.seq = 0;
-                tk.slice = split > 1 ? q : -1;
+                tk.slice = next_slot + q;
                 tk.from_c = q == 0 ? 1 : 0;
                 T.push_back(tk);
             }
-        if (split > 1) {
-            // slices beyond the last non-empty one never get written
-            const int used = static_cast<int>(cdiv(e.k, per));
-            s->slices = used;
-            s->work_ld = e.m;
-            s->work_slice = e.m * e.n;
-            cuda_check(cudaMalloc(&s->work, sizeof(double) * static_cast<std::size_t>(s->work_slice) * used),
-                       "cudaMalloc(split-k workspace)");
-            if (used == 1)
-                for (auto& tk : T) tk.slice = -1;
-            if (used == 1) s->slices = 1;
+            next_slot += used;
         }
+        s->slices = static_cast<int>(red.size());
+        if (!red.empty()) {
+            s->work_ld = info.tile_m;
+            s->work_slice = static_cast<i64>(info.tile_m) * info.tile_n;
+            cuda_check(cudaMalloc(&s->work, sizeof(double) * static_cast<std::size_t>(s->work_slice) * next_slot),
+                       "cudaMalloc(split-k workspace)");
+            cuda_check(cudaMalloc(&s->reduce, sizeof(gpu::ReduceTile) * red.size()), "cudaMalloc(reduce list)");
+            cuda_check(cudaMemcpyAsync(s->reduce, red.data(), sizeof(gpu::ReduceTile) * red.size(),
+                                       cudaMemcpyHostToDevice, stream),
+                       "upload reduce list");
+            cuda_check(cudaStreamSynchronize(stream), "upload reduce list (sync)");
+        }
+        }  // uniform / tail split
     } else if (o.schedule == TM_SCHEDULE_FAITHFUL) {
         const i64 cells = nest.cells();
         if (cells > 64LL * 1000 * 1000) fail_usage("faithful schedule limited to 64M cells; use the fused schedule");
@@ -297,6 +418,7 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
     int grid = o.ctas > 0 ? std::min(o.ctas, slots) : slots;
     s->grid = std::max(1, std::min<int>(grid, static_cast<int>(T.size())));
     if (pair) s->grid = 2 * std::max(1, std::min<int>(slots / 2, static_cast<int>(T.size())));  // clusters of 2
+    if (s->blocked) s->grid = s->grid_fixed;  // one task range per CTA
     cuda_check(cudaGetDevice(&s->device), "cudaGetDevice");
     cuda_check(cudaMalloc(&s->tasks, sizeof(gpu::Task) * std::max<std::size_t>(1, T.size())), "cudaMalloc(tasks)");
     // Stream-ordered upload, completed before the schedule is used: a plain
@@ -335,11 +457,11 @@ void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t l
         cuda_check(cudaMemsetAsync(s.progress, 0, sizeof(int32_t) * static_cast<std::size_t>(s.regions), stream),
                    "reset progress");
     gpu::Args a{A, lda, B, ldb, C, ldc, s.tasks, static_cast<int32_t>(s.host_tasks.size()), s.progress, s.work,
-                s.work_ld, s.work_slice};
+                s.work_ld, s.work_slice, s.blocked ? s.cta_first : nullptr};
     cuda_check(gpu::launch(s.kernel, vec16, a, s.grid, stream), "task kernel launch");
     int launches = 1;
-    if (s.slices > 1) {
-        cuda_check(gpu::launch_reduce(C, ldc, s.work, s.work_ld, s.work_slice, s.slices, e.m, e.n, stream),
+    if (s.slices > 0) {
+        cuda_check(gpu::launch_reduce_tiles(C, ldc, s.work, s.work_ld, s.work_slice, s.reduce, s.slices, stream),
                    "split-k reduce launch");
         ++launches;
     }

@@ -76,6 +76,7 @@ struct Dest {
     const double* src;  // nullptr: start from zero
     double* dst;
     int64_t ld_src, ld_dst;
+    int64_t oi, oj;     // destination coordinates of the task's (0, 0)
 };
 __device__ __forceinline__ Dest resolve(const Args& a, const Task& t) {
     Dest d;
@@ -83,11 +84,15 @@ __device__ __forceinline__ Dest resolve(const Args& a, const Task& t) {
         d.src = a.C;
         d.dst = a.C;
         d.ld_src = d.ld_dst = a.ldc;
-    } else {
+        d.oi = t.i0;
+        d.oj = t.j0;
+    } else {  // a k-part of a split tile: partial into its compact slot
         d.src = t.from_c ? a.C : nullptr;
         d.ld_src = a.ldc;
         d.dst = a.work + static_cast<int64_t>(t.slice) * a.work_slice;
         d.ld_dst = a.work_ld;
+        d.oi = 0;
+        d.oj = 0;
     }
     return d;
 }
@@ -261,7 +266,10 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
     const int g = lane >> 2, tq = lane & 3;
     const int wm0 = (warp % NWM) * WM, wn0 = (warp / NWM) * WN;
 
-    for (int ti = blockIdx.x; ti < a.ntasks; ti += gridDim.x) {
+    const int t_lo = a.cta_first ? a.cta_first[blockIdx.x] : static_cast<int>(blockIdx.x);
+    const int t_hi = a.cta_first ? a.cta_first[blockIdx.x + 1] : a.ntasks;
+    const int t_step = a.cta_first ? 1 : static_cast<int>(gridDim.x);
+    for (int ti = t_lo; ti < t_hi; ti += t_step) {
         const Task t = a.tasks[ti];
         wait_turn(a, t);
         const int nk = (t.k + BK - 1) / BK;
@@ -331,7 +339,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
         cp_wait<0>();
         __syncthreads();
 
-        const int64_t di = t.i0, dj = t.j0;
+        const int64_t di = d.oi, dj = d.oj;
 #pragma unroll
         for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
@@ -357,7 +365,10 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN)) k_simt(Args a) {
     const int tx = threadIdx.x % NTX, ty = threadIdx.x / NTX;
     const int r0 = ty * TM, c0 = tx * TN;
 
-    for (int ti = blockIdx.x; ti < a.ntasks; ti += gridDim.x) {
+    const int t_lo = a.cta_first ? a.cta_first[blockIdx.x] : static_cast<int>(blockIdx.x);
+    const int t_hi = a.cta_first ? a.cta_first[blockIdx.x + 1] : a.ntasks;
+    const int t_step = a.cta_first ? 1 : static_cast<int>(gridDim.x);
+    for (int ti = t_lo; ti < t_hi; ti += t_step) {
         const Task t = a.tasks[ti];
         wait_turn(a, t);
         const int nk = (t.k + kBK - 1) / kBK;
@@ -423,22 +434,24 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN)) k_simt(Args a) {
             for (int j = 0; j < TN; ++j) {
                 const int r = r0 + i, c = c0 + j;
                 if (r < t.m && c < t.n)
-                    d.dst[(static_cast<int64_t>(t.i0) + r) + (static_cast<int64_t>(t.j0) + c) * d.ld_dst] = acc[i][j];
+                    d.dst[(d.oi + r) + (d.oj + c) * d.ld_dst] = acc[i][j];
             }
         signal_done(a, t);
     }
 }
 
-// Deterministic split-k reduction: C = W[0] + W[1] + ... in slice order.
-__global__ void k_reduce(double* C, int64_t ldc, const double* W, int64_t wld, int64_t wslice, int slices, int64_t m,
-                         int64_t n) {
-    const int64_t total = m * n;
-    for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < total;
-         x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = x % m, j = x / m;
-        double s = W[i + j * wld];
-        for (int q = 1; q < slices; ++q) s = __dadd_rn(s, W[q * wslice + i + j * wld]);
-        C[i + j * ldc] = s;
+// Deterministic split-k reduction, one CTA per split tile:
+// C(tile) = slot0 + slot1 + ... in slot order.
+__global__ void k_reduce_tiles(double* C, int64_t ldc, const double* W, int64_t wld, int64_t wslot,
+                               const ReduceTile* tiles) {
+    const ReduceTile rt = tiles[blockIdx.x];
+    const int64_t total = static_cast<int64_t>(rt.m) * rt.n;
+    const double* base = W + static_cast<int64_t>(rt.slot0) * wslot;
+    for (int64_t x = threadIdx.x; x < total; x += blockDim.x) {
+        const int64_t i = x % rt.m, j = x / rt.m;
+        double s = base[i + j * wld];
+        for (int q = 1; q < rt.nslots; ++q) s = __dadd_rn(s, base[q * wslot + i + j * wld]);
+        C[(rt.i0 + i) + (rt.j0 + j) * ldc] = s;
     }
 }
 
@@ -548,11 +561,10 @@ cudaError_t launch(Kernel kernel, bool vec16, const Args& args, int grid, cudaSt
     return cudaLaunchKernel(en.fn[vec16], dim3(grid), dim3(en.threads), params, en.smem, stream);
 }
 
-cudaError_t launch_reduce(double* C, int64_t ldc, const double* work, int64_t work_ld, int64_t work_slice, int slices,
-                          int64_t m, int64_t n, cudaStream_t stream) {
-    const int64_t total = m * n;
-    int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-    k_reduce<<<blocks, 256, 0, stream>>>(C, ldc, work, work_ld, work_slice, slices, m, n);
+cudaError_t launch_reduce_tiles(double* C, int64_t ldc, const double* work, int64_t work_ld, int64_t work_slice,
+                                const ReduceTile* tiles, int ntiles, cudaStream_t stream) {
+    if (ntiles <= 0) return cudaSuccess;
+    k_reduce_tiles<<<ntiles, 512, 0, stream>>>(C, ldc, work, work_ld, work_slice, tiles);
     return cudaGetLastError();
 }
 

@@ -32,9 +32,18 @@ struct Args {
     const Task* tasks;
     int32_t ntasks;
     int32_t* progress;   // one counter per ordered region (faithful schedule)
-    double* work;        // split-k slices, column-major m x n each, ld = work_ld
+    double* work;        // split-k partials: one compact slot per (tile, k-part), tile-local, ld = work_ld
     int64_t work_ld;
-    int64_t work_slice;  // elements per slice
+    int64_t work_slice;  // elements per slot
+    const int32_t* cta_first;  // blocked assignment: CTA c runs tasks [cta_first[c], cta_first[c+1]);
+                               // nullptr = strided (task t on CTA t mod grid)
+};
+
+// One k-split C tile: its partials live in slots slot0 .. slot0+nslots-1 and
+// are summed in slot order (slot0 started from C's incoming value).
+struct ReduceTile {
+    int32_t i0, j0, m, n;
+    int32_t slot0, nslots;
 };
 
 enum Kernel : int {
@@ -62,9 +71,10 @@ struct KernelInfo {
 cudaError_t launch(Kernel kernel, bool vec16, const Args& args, int grid, cudaStream_t stream);
 // Occupancy-derived info (queries the device on first call).
 cudaError_t kernel_info(Kernel kernel, KernelInfo* info);
-// C = sum over slices in slice order (deterministic split-k reduction).
-cudaError_t launch_reduce(double* C, int64_t ldc, const double* work, int64_t work_ld, int64_t work_slice,
-                          int slices, int64_t m, int64_t n, cudaStream_t stream);
+// C(tile) = slot0 + slot1 + ... in slot order for every listed tile
+// (deterministic split-k reduction).
+cudaError_t launch_reduce_tiles(double* C, int64_t ldc, const double* work, int64_t work_ld, int64_t work_slice,
+                                const ReduceTile* tiles, int ntiles, cudaStream_t stream);
 // Sustained FP64 DMMA rate of this device (TFLOP/s) over `launches` probe launches.
 cudaError_t measure_fp64_peak(int launches, double* tflops);
 // tcgen05 BF16/TF32-input GEMM over a task list (C fp32, column-major).

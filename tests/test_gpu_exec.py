@@ -302,3 +302,36 @@ def test_multigpu_driver_world1_nccl():
         assert ok, worst
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("split", [0, 3, -1])
+def test_split_k_tail_and_uniform(split):
+    """split_k=-1 (stream-K: equal contiguous (tile, k-slab) ranges per CTA),
+    split_k=0 (auto; stream-K for this ragged 256-tile grid), split_k=3
+    (every tile in 3 parts). All reduce the cut tiles in a fixed slot order:
+    within the bound and bitwise reproducible run to run."""
+    m = n = k = 2048
+    hier = T.gpu_hierarchy(128)
+    d = T.parse_name("C2A1C0")
+    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(128, 128)),
+                             pinned=T.BlocksizeSet({(1, "m"): 128}))
+    nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+    a, b, c = O.fill_uniform(41, [(m, k), (k, n), (m, n)])
+    got1 = run_gpu(nest, a, b, c, split_k=split)
+    launch = nest.last_launch()
+    assert launch["launches"] == 2  # task kernel + tile reduction
+    assert launch["tasks"] > 256
+    got2 = run_gpu(nest, a, b, c, split_k=split)
+    assert np.array_equal(got1, got2)
+    rng = np.random.default_rng(9)
+    ii, jj = rng.integers(0, m, 4096), rng.integers(0, n, 4096)
+    want, ab = O.entries(k, a, m, b, k, c, m, ii, jj)
+    ok, worst = H.entrywise_ok(got1[ii + jj * m], want, ab, k, c0=c[ii + jj * m])
+    assert ok, worst
+    # exact numerics ignore auto-splitting and stay bitwise equal to the reference
+    if split == 0:
+        ex = run_gpu(nest, a, b, c, numerics="exact", split_k=0)
+        assert nest.last_launch()["launches"] == 1
+        want_all = c.copy()
+        O.execute_nest(m, n, k, [(L.dim, L.blocksize) for L in nest.loops], nest.m_r, nest.n_r, a, b, want_all)
+        assert np.array_equal(ex, want_all)

@@ -26,7 +26,8 @@ MEMBERS_L2 = ["A2C0", "B2C0"]
 
 
 def cases(quick: bool):
-    out = [("config1", (2048, 2048, 2048), ["C2A1C0"], {"c_zero": True})]
+    out = [("config1", (2048, 2048, 2048), ["C2A1C0"], {"c_zero": True}),
+           ("config1_no_split", (2048, 2048, 2048), ["C2A1C0"], {"c_zero": True, "split_k": 1})]
     sizes = [4096, 8192] if quick else [4096, 8192, 16384]
     for s in sizes:
         out.append(("config2", (s, s, s), MEMBERS_L2L1 + MEMBERS_L2, {}))
@@ -96,7 +97,7 @@ def main():
                     C.zero_()
                 else:
                     T.fill_uniform_device(C, 3)
-                opts = T.ExecOptions(numerics="dmma", schedule=sched, split_k=extra.get("split_k", 1), tile=tm,
+                opts = T.ExecOptions(numerics="dmma", schedule=sched, split_k=extra.get("split_k", 0), tile=tm,
                                      tile_n=tn)
                 rep = nest.model()
                 rec["blocksizes"] = {f"{lv}:{d}": v for (lv, d), v in bs.entries()}
