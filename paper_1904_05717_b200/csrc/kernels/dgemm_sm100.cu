@@ -290,18 +290,30 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
         }
 
         const Dest d = resolve(a, t);
+        // The MMA computes the transposed tile (D' = B^T A^T, operands
+        // swapped): lane (g, tq) then holds C rows wm0+mi*8+2tq+{0,1} of
+        // column wn0+ni*8+g — two consecutive column-major elements, so the C
+        // tile moves with one 16-byte access per pair instead of two 8-byte
+        // ones (same products, same k order).
         double acc[FM][FN][2];
+        const bool src_vec = d.src != nullptr && ((reinterpret_cast<uintptr_t>(d.src) & 15) | (d.ld_src & 1) |
+                                                  (static_cast<int64_t>(t.i0) & 1)) == 0;
 #pragma unroll
         for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < FN; ++ni)
+            for (int ni = 0; ni < FN; ++ni) {
+                const int r = wm0 + mi * 8 + 2 * tq, c = wn0 + ni * 8 + g;
+                const double* p = d.src + (t.i0 + r) + static_cast<int64_t>(t.j0 + c) * d.ld_src;
+                if (src_vec && r + 1 < t.m && c < t.n) {
+                    const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+                    acc[mi][ni][0] = v.x;
+                    acc[mi][ni][1] = v.y;
+                } else {
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int r = wm0 + mi * 8 + g, c = wn0 + ni * 8 + 2 * tq + e;
-                    acc[mi][ni][e] = (d.src && r < t.m && c < t.n)
-                                         ? __ldcg(d.src + (t.i0 + r) + static_cast<int64_t>(t.j0 + c) * d.ld_src)
-                                         : 0.0;
+                    for (int e = 0; e < 2; ++e)
+                        acc[mi][ni][e] = (d.src && r + e < t.m && c < t.n) ? __ldcg(p + e) : 0.0;
                 }
+            }
 
         for (int s = 0; s < nk; ++s) {
             cp_wait<STAGES - 2>();
@@ -320,7 +332,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
 #pragma unroll
                 for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-                    for (int ni = 0; ni < FN; ++ni) dmma884(acc[mi][ni], af[mi], bf[ni]);
+                    for (int ni = 0; ni < FN; ++ni) dmma884(acc[mi][ni], bf[ni], af[mi]);
                 // stage the slab STAGES-1 ahead between the DMMA groups
                 if (kk == 0 && nx < nk) {
                     if constexpr (V16) {
@@ -340,15 +352,21 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
         __syncthreads();
 
         const int64_t di = d.oi, dj = d.oj;
+        const bool dst_vec = ((reinterpret_cast<uintptr_t>(d.dst) & 15) | (d.ld_dst & 1) | (di & 1)) == 0;
 #pragma unroll
         for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < FN; ++ni)
+            for (int ni = 0; ni < FN; ++ni) {
+                const int r = wm0 + mi * 8 + 2 * tq, c = wn0 + ni * 8 + g;
+                double* p = d.dst + (di + r) + (dj + c) * d.ld_dst;
+                if (dst_vec && r + 1 < t.m && c < t.n) {
+                    *reinterpret_cast<double2*>(p) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+                } else {
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int r = wm0 + mi * 8 + g, c = wn0 + ni * 8 + 2 * tq + e;
-                    if (r < t.m && c < t.n) d.dst[(di + r) + (dj + c) * d.ld_dst] = acc[mi][ni][e];
+                    for (int e = 0; e < 2; ++e)
+                        if (r + e < t.m && c < t.n) p[e] = acc[mi][ni][e];
                 }
+            }
         signal_done(a, t);
     }
 }
