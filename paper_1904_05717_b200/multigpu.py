@@ -95,8 +95,11 @@ class Summa:
         self.r, self.c = lay.coords(rank)
         self.dist = dist
         self.row_group, self.col_group = row_group, col_group
-        self.abuf = [torch.empty(lay.mL * lay.KC, dtype=torch.float64, device=device) for _ in range(2)]
-        self.bbuf = [torch.empty(lay.KC * lay.nL, dtype=torch.float64, device=device) for _ in range(2)]
+        # receive buffers only where chunks actually arrive from peers
+        self.abuf = [torch.empty(lay.mL * lay.KC, dtype=torch.float64, device=device)
+                     for _ in range(2 if lay.Pc > 1 else 0)]
+        self.bbuf = [torch.empty(lay.KC * lay.nL, dtype=torch.float64, device=device)
+                     for _ in range(2 if lay.Pr > 1 else 0)]
         self.exchanged_bytes = 0
 
     @staticmethod
