@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--size", type=int, default=M, help="square size (default 16384 = configs[1] max)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--summa", action="store_true",
+                   help="run the multi-GPU 2-D partition driver even at N=1 (exercises the N>1 code path)")
     return p.parse_args()
 
 
@@ -229,8 +231,10 @@ def our_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world > 1 or args.summa:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29541")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
         from paper_1904_05717_b200 import multigpu
 
         return multigpu.bench(args, T, make_plan, world, rank, local)
