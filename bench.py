@@ -211,14 +211,14 @@ def reference_arm(args):
 
 # ------------------------------------------------------------------ our arm
 def make_plan(T, m, n, k, tile=128):
-    hier = T.gpu_hierarchy(tile)
-    d = T.parse_name(FAMILY)
-    # L2 plan: a wave-sized C block (12 x 12 CTA tiles of 128^2 ~ one wave on
-    # 148 SMs), so the tiles that share the L2-resident block run together.
-    pins = T.BlocksizeSet({(1, "m"): tile, (2, "m"): min(m, 12 * tile), (2, "n"): min(n, 12 * tile)})
-    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(tile, tile)),
-                             pinned=pins)
-    return T.build_plan(d, bs, hier, T.Shape(m, n, k)), bs, hier
+    """C2A1C0 on the B200 hierarchy with the L2 level at its effective
+    capacity for residency (planner.L2_EFFECTIVE, measured), blocksizes from
+    the reference's derivation with the GPU pins (planner.derive_for_gpu)."""
+    from paper_1904_05717_b200 import planner as P
+
+    hier = P.gpu_hierarchy_effective(tile)
+    bs = P.derive_for_gpu(FAMILY, (m, n, k), hier, (tile, tile))
+    return T.build_plan(T.parse_name(FAMILY), bs, hier, T.Shape(m, n, k)), bs, hier
 
 
 def our_arm(args):
@@ -320,7 +320,9 @@ def our_arm(args):
                    "blocksizes": {f"{lv}:{d}": v for (lv, d), v in bs.entries()},
                    "schedule": "fused", "numerics": "dmma (mma.sync m8n8k4 f64)", "cta_tile": "128x128",
                    "split_k": "auto (tail split of the last partial wave)",
-                   "l2_flush": "not needed: inputs 6.4 GB > 126 MB L2", "parallelism": "1 GPU"},
+                   "l2_flush": "not needed: inputs 6.4 GB > 126 MB L2", "parallelism": "1 GPU",
+                   "hierarchy_elements": [hier.capacity(i) for i in range(hier.size())],
+                   "l2_effective_fraction": 0.25},
         "pct_of_fp64_peak": 100.0 * value / peak,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,

@@ -22,6 +22,24 @@ from . import tilemul as T
 # (SURVEY.md §7.1): two cache levels, or one with the SMEM level skipped.
 GPU_MEMBERS = ("C2A1C0", "C2B1C0", "B2A1C0", "A2B1C0", "A2C0", "B2C0")
 WAVE_TILES = 12  # an L2 block side of 12 CTA tiles: 144 tiles ~ one wave on 148 SMs
+# Effective L2 capacity for MOMMS residency, as a fraction of the physical
+# 126 MiB. Measured (profiles/model_check_r01_l2frac_*.json): with the L2
+# level sized at 100% or 50%, C blocks derived by the reference's fit rules
+# do not stay resident (faithful C2A1C0 at 8192^3 moves 17x / 3.1x the
+# modelled HBM bytes); at 25% every faithful member lands within 0.95-1.03x
+# of the model and the fused schedule within 0.81-1.26x. The L2 is split
+# over two dies and also holds the streamed panels, so ~1/4 of it is what a
+# resident block can count on.
+L2_EFFECTIVE = 0.25
+
+
+def gpu_hierarchy_effective(tile: int = 128, l2_fraction: float = L2_EFFECTIVE) -> T.CacheHierarchy:
+    """The current device's {CTA tile, SMEM, L2} hierarchy with the L2 level
+    at its effective capacity for residency."""
+    h = T.gpu_hierarchy(tile)
+    caps = [h.capacity(i) for i in range(h.size())]
+    caps[-1] = max(caps[-2] + 1, int(caps[-1] * l2_fraction))
+    return T.CacheHierarchy.from_capacities(caps)
 
 
 @dataclass
@@ -86,11 +104,11 @@ def rank_members(shape: Tuple[int, int, int], hier: T.CacheHierarchy, members=GP
 
 
 def select_for_gpu(shape: Tuple[int, int, int], hier: Optional[T.CacheHierarchy] = None, tile=(128, 128),
-                   wave_block: bool = True):
+                   wave_block: bool = False):
     """The cheapest member by the model, with the plan built: (nest, candidate).
     Ties (equal modelled bytes) go to the member whose outermost resident the
     reference's select_algorithm picks."""
-    hier = hier or T.gpu_hierarchy(tile[0])
+    hier = hier or gpu_hierarchy_effective(tile[0])
     ranked = rank_members(shape, hier, tile=tile, wave_block=wave_block)
     best = [c for c in ranked if c.blocksizes is not None]
     if not best:

@@ -37,8 +37,15 @@ def cases(quick: bool):
     return out
 
 
+L2_FRAC = 1.0
+
+
 def plan_for(T, name, shape, tile=128):
     hier = T.gpu_hierarchy(tile)
+    if L2_FRAC != 1.0:  # model an effective L2 capacity (fraction of the physical one) for residency
+        caps = [hier.capacity(i) for i in range(hier.size())]
+        caps[-1] = int(caps[-1] * L2_FRAC)
+        hier = T.CacheHierarchy.from_capacities(caps)
     d = T.parse_name(name)
     pins = {}
     lv1 = d.plan_at(1)
@@ -68,25 +75,35 @@ def main():
     ap.add_argument("--once", action="store_true")
     ap.add_argument("--schedules", default="fused")
     ap.add_argument("--tiles", default="128x128,128x64")
+    ap.add_argument("--only", default="", help="comma-separated config names to run (default: all)")
+    ap.add_argument("--members", default="", help="comma-separated family members (default: per config)")
+    ap.add_argument("--l2-frac", type=float, default=1.0, help="effective L2 capacity fraction for derivation")
     a = ap.parse_args()
     import torch
 
     from paper_1904_05717_b200 import tilemul as T
 
     peak = None if a.once else T.measure_fp64_peak(20)
+    only = set(x for x in a.only.split(",") if x)
+    global L2_FRAC
+    L2_FRAC = a.l2_frac
+    keep = [x for x in a.members.split(",") if x]
     for cfg, shape, members, extra in cases(a.quick):
+        if only and cfg not in only:
+            continue
         m, n, k = shape
         A = torch.empty(m * k, dtype=torch.float64, device="cuda")
         B = torch.empty(k * n, dtype=torch.float64, device="cuda")
         C = torch.empty(m * n, dtype=torch.float64, device="cuda")
         T.fill_uniform_device(A, 1)
         T.fill_uniform_device(B, 2)
-        for name in members:
+        for name in (keep or members):
             for sched, tile in [(sc, tl) for sc in a.schedules.split(",") for tl in a.tiles.split(",")]:
                 if sched == "faithful" and tile != a.tiles.split(",")[0]:
                     continue
                 tm, tn = (int(x) for x in tile.split("x"))
-                rec = {"config": cfg, "shape": shape, "family": name, "schedule": sched, "cta_tile": tile}
+                rec = {"config": cfg, "shape": shape, "family": name, "schedule": sched, "cta_tile": tile,
+                       "l2_frac": L2_FRAC}
                 try:
                     nest, bs, hier = plan_for(T, name, shape)
                 except Exception as e:  # infeasible on this hierarchy: reported, not hidden
@@ -108,6 +125,7 @@ def main():
                     print(json.dumps(rec), flush=True)
                     continue
                 if a.once:
+                    opts.split_k = 1 if extra.get("split_k", 0) == 0 and sched == "fused" and cfg != "config3b_inner_product" else opts.split_k
                     T.execute(nest, A, B, C, opts)
                     torch.cuda.synchronize()
                     rec["launch"] = nest.last_launch()
