@@ -171,6 +171,19 @@ int tm_execute_tc(tm_plan* plan, int dtype, const void* A, int64_t lda, const vo
 /* Device rounding of FP64 inputs: to BF16 (RNE; y is uint16 storage) or to
  * TF32 values in fp32 storage (RNE to 11 significant bits). */
 int tm_round_inputs(int dtype, const double* x, void* y, int64_t count, void* stream);
+/* --- prepacked ("hierarchical") operand layouts (layout.hpp:17-145, plan.hpp:113-124) --- */
+/* BlockLayout::element_address for a cut chain (on_rows[s], sizes[s]), outermost first. */
+int tm_layout_address(int64_t rows, int64_t cols, const int32_t* on_rows, const int64_t* sizes, int ncuts, int64_t i,
+                      int64_t j, int64_t* address);
+/* layout_for(nest, operand): the plan's hierarchical layout of 'A', 'B' or 'C'. */
+int tm_plan_layout(const tm_plan* plan, char operand, int32_t* on_rows, int64_t* sizes, int cap, int* ncuts);
+/* pack / unpack on the device (column-major <-> the plan's layout of the operand). */
+int tm_pack(const tm_plan* plan, char operand, const double* colmajor, double* packed, void* stream);
+int tm_unpack(const tm_plan* plan, char operand, const double* packed, double* colmajor, void* stream);
+/* execute() on device buffers prepacked in the plan's layouts (exec.hpp:94-138 with
+ * blocked MatrixBuffers): relaid to column-major scratch, executed, C packed back. */
+int tm_execute_packed(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts* opts,
+                      void* stream);
 /* Number of CTA tasks and kernel launches the last tm_execute issued. */
 int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, int32_t* ctas);
 

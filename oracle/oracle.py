@@ -103,6 +103,7 @@ def ref():
         L.ref_streaming_efficiency.restype = C.c_double
         L.ref_goto_efficiency.argtypes = [C.c_int64, C.c_int64]
         L.ref_goto_efficiency.restype = C.c_double
+        L.ref_pack.argtypes = [cp] + hier + bs + [C.c_char, C.c_void_p, C.c_void_p, C.c_char_p, C.c_int]
         L.ref_select.argtypes = [C.c_int64] * 4
         L.ref_select.restype = C.c_char
         _ref = L
@@ -257,3 +258,15 @@ def counter_uniform(seed: int, index):
         z = z ^ (z >> np.uint64(31))
     u = (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
     return 2.0 * u - 1.0
+
+
+def ref_pack(name, caps, shape, bs, op, src, inclusive=None):
+    """The reference's pack(src, nest) of operand `op` (column-major -> layout_for)."""
+    L = ref()
+    dst = np.empty_like(src)
+    err = C.create_string_buffer(4096)
+    rc = L.ref_pack(name.encode(), *_hier_args(caps, inclusive), *shape, *_bs_args(bs), op.encode(), src.ctypes.data,
+                    dst.ctypes.data, err, 4096)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    return dst

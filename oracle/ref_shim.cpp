@@ -256,6 +256,22 @@ double ref_streaming_efficiency(char variant, int64_t b1, int64_t b2) {
 
 double ref_goto_efficiency(int64_t kc, int64_t nc) { return goto_efficiency(kc, nc); }
 
+// pack(src, nest) for one operand (plan.hpp:122-124 / layout.hpp:122-135):
+// column-major src -> dst in layout_for(nest, op).
+int ref_pack(const char* name, const int64_t* caps, const int* inclusive, int nlev, int64_t m, int64_t n, int64_t k,
+             const int* lvl, const char* dim, const int64_t* val, int nbs, char op, const double* src, double* dst,
+             char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        LoopNest nest = build_plan(parse_name(name), make_bs(lvl, dim, val, nbs), make_hier(caps, inclusive, nlev),
+                                   Shape(m, n, k));
+        Operand o = operand_from_char(op);
+        MatrixBuffer b = MatrixBuffer::column_major(o, nest.shape.rows(o), nest.shape.cols(o));
+        std::memcpy(b.data.data(), src, sizeof(double) * b.data.size());
+        MatrixBuffer p = pack(b, nest);
+        std::memcpy(dst, p.data.data(), sizeof(double) * p.data.size());
+    });
+}
+
 char ref_select(int64_t m, int64_t n, int64_t k, int64_t cap) { return to_char(select_algorithm(Shape(m, n, k), cap)); }
 
 }  // extern "C"

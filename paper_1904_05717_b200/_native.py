@@ -74,6 +74,11 @@ SIGNATURES = [
     ("tm_execute_host", C.c_int, [P, P, P, P, C.POINTER(tm_exec_opts)]),
     ("tm_execute_tc", C.c_int, [P, C.c_int, P, i64, P, i64, P, i64, C.POINTER(tm_exec_opts), P]),
     ("tm_round_inputs", C.c_int, [C.c_int, P, P, i64, P]),
+    ("tm_layout_address", C.c_int, [i64, i64, C.POINTER(i32), C.POINTER(i64), C.c_int, i64, i64, C.POINTER(i64)]),
+    ("tm_plan_layout", C.c_int, [P, C.c_char, C.POINTER(i32), C.POINTER(i64), C.c_int, C.POINTER(C.c_int)]),
+    ("tm_pack", C.c_int, [P, C.c_char, P, P, P]),
+    ("tm_unpack", C.c_int, [P, C.c_char, P, P, P]),
+    ("tm_execute_packed", C.c_int, [P, P, P, P, C.POINTER(tm_exec_opts), P]),
     ("tm_plan_last_launch", C.c_int, [P, C.POINTER(i64), C.POINTER(i32), C.POINTER(i32)]),
     ("tm_fill_seeded", C.c_int, [C.c_uint64, P, i64, P, i64, P, i64]),
     ("tm_measure_fp64_peak", C.c_int, [C.c_int, C.POINTER(dbl)]),

@@ -175,6 +175,10 @@ gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o) {
     switch (o.numerics) {
         case TM_NUMERICS_DMMA:
             if (o.tile == 128 && tn == 64) return gpu::kDmma128x64;
+            // short k: every task is mostly C load/store; two CTAs per SM
+            // (128 x 64 tiles) hide one CTA's C traffic behind the other's DMMAs
+            if (o.tile == 0 && !small_tile && nest.ext.k <= 512 && o.schedule == TM_SCHEDULE_FUSED)
+                return gpu::kDmma128x64;
             return small_tile ? gpu::kDmma64 : gpu::kDmma128;
         case TM_NUMERICS_FMA:
             if (tn == 64 && o.tile == 128) fail_usage("fma numerics run on square tiles");
@@ -827,6 +831,89 @@ int tm_round_inputs(int dtype, const double* x, void* y, int64_t count, void* st
         if (dtype != TM_DTYPE_BF16 && dtype != TM_DTYPE_TF32) fail_usage("dtype must be TM_DTYPE_BF16 or TM_DTYPE_TF32");
         cuda_check(gpu::launch_round(dtype == TM_DTYPE_TF32, x, y, count, static_cast<cudaStream_t>(stream)),
                    "round launch");
+    });
+}
+
+// ------------------------------------------------------ prepacked layouts
+
+namespace {
+
+gpu::LayoutDev layout_dev(const Blocked& b) {
+    if (static_cast<int>(b.cuts.size()) > gpu::LayoutDev::kMaxCuts) fail_usage("too many partition steps");
+    gpu::LayoutDev L{};
+    L.rows = b.rows;
+    L.cols = b.cols;
+    L.ncuts = static_cast<int32_t>(b.cuts.size());
+    for (std::size_t s = 0; s < b.cuts.size(); ++s) {
+        L.on_rows[s] = b.cuts[s].rows ? 1 : 0;
+        L.size[s] = b.cuts[s].size;
+    }
+    return L;
+}
+
+}  // namespace
+
+int tm_layout_address(int64_t rows, int64_t cols, const int32_t* on_rows, const int64_t* sizes, int ncuts, int64_t i,
+                      int64_t j, int64_t* address) {
+    return guard([&] {
+        std::vector<Cut> cuts;
+        for (int s = 0; s < ncuts; ++s) cuts.push_back(Cut{on_rows[s] != 0, sizes[s]});
+        *address = make_blocked(rows, cols, std::move(cuts)).address(i, j);
+    });
+}
+
+int tm_plan_layout(const tm_plan* plan, char operand, int32_t* on_rows, int64_t* sizes, int cap, int* ncuts) {
+    return guard([&] {
+        if (!plan) fail_usage("null plan");
+        const Blocked b = layout_of(plan->nest, opnd_of_char(operand));
+        if (ncuts) *ncuts = static_cast<int>(b.cuts.size());
+        if (static_cast<int>(b.cuts.size()) > cap) fail_usage("cut buffer too small");
+        for (std::size_t s = 0; s < b.cuts.size(); ++s) {
+            on_rows[s] = b.cuts[s].rows ? 1 : 0;
+            sizes[s] = b.cuts[s].size;
+        }
+    });
+}
+
+int tm_pack(const tm_plan* plan, char operand, const double* colmajor, double* packed, void* stream) {
+    return guard([&] {
+        if (!plan || !colmajor || !packed) fail_usage("null argument");
+        cuda_check(gpu::launch_relayout(colmajor, packed, layout_dev(layout_of(plan->nest, opnd_of_char(operand))),
+                                        true, static_cast<cudaStream_t>(stream)),
+                   "pack launch");
+    });
+}
+
+int tm_unpack(const tm_plan* plan, char operand, const double* packed, double* colmajor, void* stream) {
+    return guard([&] {
+        if (!plan || !colmajor || !packed) fail_usage("null argument");
+        cuda_check(gpu::launch_relayout(packed, colmajor, layout_dev(layout_of(plan->nest, opnd_of_char(operand))),
+                                        false, static_cast<cudaStream_t>(stream)),
+                   "unpack launch");
+    });
+}
+
+int tm_execute_packed(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts* opts,
+                      void* stream) {
+    return guard([&] {
+        if (!plan) fail_usage("null plan");
+        if (!A || !B || !C) fail_usage("null operand pointer");
+        const Extents& e = plan->nest.ext;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const std::size_t na = static_cast<std::size_t>(e.m * e.k), nb = static_cast<std::size_t>(e.k * e.n),
+                          nc = static_cast<std::size_t>(e.m * e.n);
+        if (!plan->dA) {
+            cuda_check(cudaMalloc(&plan->dA, na * sizeof(double)), "cudaMalloc(A)");
+            cuda_check(cudaMalloc(&plan->dB, nb * sizeof(double)), "cudaMalloc(B)");
+            cuda_check(cudaMalloc(&plan->dC, nc * sizeof(double)), "cudaMalloc(C)");
+        }
+        // the kernels stage column-major k-slabs; prepacked operands are
+        // relaid once per call (2 extra passes over A, B and C each)
+        cuda_check(gpu::launch_relayout(A, plan->dA, layout_dev(layout_of(plan->nest, kA)), false, st), "unpack A");
+        cuda_check(gpu::launch_relayout(B, plan->dB, layout_dev(layout_of(plan->nest, kB)), false, st), "unpack B");
+        cuda_check(gpu::launch_relayout(C, plan->dC, layout_dev(layout_of(plan->nest, kC)), false, st), "unpack C");
+        run(plan, plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, opts, st);
+        cuda_check(gpu::launch_relayout(plan->dC, C, layout_dev(layout_of(plan->nest, kC)), true, st), "pack C");
     });
 }
 

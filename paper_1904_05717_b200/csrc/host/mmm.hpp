@@ -212,3 +212,26 @@ double roofline(double intensity, double peak, double bandwidth);
 void fill_seeded(uint64_t seed, double* a, int64_t na, double* b, int64_t nb, double* c, int64_t nc);
 
 }  // namespace mmm
+
+// ----------------------------------------------------------------- layouts
+// layout.hpp:17-98, plan.hpp:113-119: a hierarchical ("prepacked") storage
+// layout as a chain of partition steps, outermost first; each step cuts the
+// current block along rows or columns; blocks of a cut are stored
+// contiguously in partition order; the innermost block is column-major.
+namespace mmm {
+
+struct Cut {
+    bool rows = true;
+    i64 size = 1;
+};
+
+struct Blocked {
+    i64 rows = 1, cols = 1;
+    std::vector<Cut> cuts;
+    bool blocked() const { return !cuts.empty(); }
+    i64 address(i64 i, i64 j) const;  // bijection onto [0, rows*cols)
+};
+Blocked make_blocked(i64 rows, i64 cols, std::vector<Cut> cuts);  // same-axis cuts must divide
+Blocked layout_of(const Nest& nest, Opnd op);                      // layout_for
+
+}  // namespace mmm

@@ -16,6 +16,7 @@
 //   k_simt<EXACT> — DMUL then DADD per (entry, k): bit-exact against the
 //                   reference's own execute() (built -O2, no FMA contraction).
 #include <cstdint>
+#include <mutex>
 
 #include "gpu.hpp"
 
@@ -540,8 +541,10 @@ const Entry kTable[kKernelCount] = {
 KernelInfo g_info[kKernelCount];
 bool g_ready[kKernelCount][2];
 int g_device = -1;
+std::mutex g_mu;  // first-use attribute setup may race between host threads
 
 cudaError_t prepare(Kernel k, bool v16) {
+    std::lock_guard<std::mutex> lk(g_mu);
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -565,7 +568,10 @@ cudaError_t prepare(Kernel k, bool v16) {
 
 cudaError_t kernel_info(Kernel kernel, KernelInfo* info) {
     cudaError_t e = prepare(kernel, false);
-    if (e == cudaSuccess) *info = g_info[kernel];
+    if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        *info = g_info[kernel];
+    }
     return e;
 }
 

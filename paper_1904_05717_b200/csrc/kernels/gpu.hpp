@@ -88,6 +88,16 @@ cudaError_t launch_tc_pair(bool tf32, const void* A, int64_t lda, const void* B,
                            int64_t m, int64_t n, int64_t k, const Task* tasks, int ntasks, int grid,
                            cudaStream_t stream);
 int tc2_smem_bytes(bool tf32);
+// A hierarchical layout for the relayout kernel (<= kMaxCuts partition steps).
+struct LayoutDev {
+    static constexpr int kMaxCuts = 24;
+    int64_t rows, cols;
+    int32_t ncuts;
+    uint8_t on_rows[kMaxCuts];
+    int64_t size[kMaxCuts];
+};
+// pack: column-major src -> blocked dst; unpack: blocked src -> column-major dst.
+cudaError_t launch_relayout(const double* src, double* dst, const LayoutDev& L, bool pack, cudaStream_t stream);
 cudaError_t launch_fill_block(double* x, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
                               int64_t col0, int64_t gld, cudaStream_t stream);
 cudaError_t launch_fill(double* x, int64_t count, uint64_t seed, uint64_t offset, cudaStream_t stream);

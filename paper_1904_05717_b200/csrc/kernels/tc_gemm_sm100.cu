@@ -17,6 +17,7 @@
 // The SMEM level of the MOMMS member is the TMA ring; the register level is
 // the TMEM accumulator (128 x 256 fp32 per tile).
 #include <cstdint>
+#include <mutex>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -520,8 +521,10 @@ __global__ void __launch_bounds__(256, 1) k_tc2(const __grid_constant__ CUtensor
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::mutex g_tc_mu;  // lazy driver-entry lookup and per-kernel attribute setup
 
 cudaError_t encoder() {
+    std::lock_guard<std::mutex> lk(g_tc_mu);
     if (g_encode) return cudaSuccess;
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -562,6 +565,7 @@ cudaError_t launch_tc_t(const void* A, int64_t lda, const void* B, int64_t ldb, 
         return e;
     if ((e = make_map(&mb, B, TF32, k, n, ldb, G::BK, kTcBN, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
     static bool attr[2] = {false, false};
+    std::lock_guard<std::mutex> lk(g_tc_mu);
     if (!attr[TF32]) {
         if ((e = cudaFuncSetAttribute(k_tc<TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM)) != cudaSuccess)
             return e;
@@ -608,6 +612,7 @@ cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb,
         return e;
     if ((e = make_map(&mb, B, TF32, k, n, ldb, G::BK, 128, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
     static bool attr[2] = {false, false};
+    std::lock_guard<std::mutex> lk(g_tc_mu);
     if (!attr[TF32]) {
         if ((e = cudaFuncSetAttribute(k_tc2<TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM)) !=
             cudaSuccess)

@@ -601,6 +601,65 @@ def fill_seeded(seed: int, shapes):
     return [x for x in arrs if x is not None]
 
 
+# ---------------------------------------------------- prepacked layouts
+@dataclass(frozen=True)
+class BlockLayout:  # layout.hpp:17-98
+    rows: int
+    cols: int
+    steps: Tuple[Tuple[bool, int], ...] = ()  # (on_rows, blocksize), outermost first
+
+    def blocked(self) -> bool:
+        return bool(self.steps)
+
+    def element_address(self, i: int, j: int) -> int:
+        n = len(self.steps)
+        on = (C.c_int32 * max(1, n))(*[int(s[0]) for s in self.steps])
+        sz = (C.c_int64 * max(1, n))(*[s[1] for s in self.steps])
+        out = C.c_int64(0)
+        _check(N.lib().tm_layout_address(self.rows, self.cols, on, sz, n, i, j, C.byref(out)))
+        return out.value
+
+
+def layout_for(nest: "LoopNest", op: str) -> BlockLayout:  # plan.hpp:113-119
+    on = (C.c_int32 * 64)()
+    sz = (C.c_int64 * 64)()
+    n = C.c_int(0)
+    _check(N.lib().tm_plan_layout(nest._ptr, op.encode(), on, sz, 64, C.byref(n)))
+    s = nest.shape
+    return BlockLayout(s.rows(op), s.cols(op), tuple((bool(on[i]), int(sz[i])) for i in range(n.value)))
+
+
+def _stream_of(stream):
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream if stream is None else getattr(stream, "cuda_stream", stream)
+
+
+def pack(x, nest: "LoopNest", op: str, stream=None):
+    """Column-major CUDA tensor -> the plan's hierarchical layout (layout.hpp:122-135)."""
+    import torch
+
+    y = torch.empty_like(x)
+    _check(N.lib().tm_pack(nest._ptr, op.encode(), x.data_ptr(), y.data_ptr(), C.c_void_p(_stream_of(stream))))
+    return y
+
+
+def unpack(x, nest: "LoopNest", op: str, stream=None):
+    """The plan's hierarchical layout -> column-major (layout.hpp:138-145)."""
+    import torch
+
+    y = torch.empty_like(x)
+    _check(N.lib().tm_unpack(nest._ptr, op.encode(), x.data_ptr(), y.data_ptr(), C.c_void_p(_stream_of(stream))))
+    return y
+
+
+def execute_packed(nest: "LoopNest", Ap, Bp, Cp, opts: ExecOptions = None, stream=None) -> None:
+    """execute() on CUDA buffers prepacked in layout_for(nest, op)."""
+    o = (opts or ExecOptions())._c()
+    _check(N.lib().tm_execute_packed(nest._ptr, Ap.data_ptr(), Bp.data_ptr(), Cp.data_ptr(), C.byref(o),
+                                     C.c_void_p(_stream_of(stream))))
+
+
 DTYPES = {"bf16": 1, "tf32": 2}
 
 

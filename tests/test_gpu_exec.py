@@ -335,3 +335,29 @@ def test_split_k_tail_and_uniform(split):
         want_all = c.copy()
         O.execute_nest(m, n, k, [(L.dim, L.blocksize) for L in nest.loops], nest.m_r, nest.n_r, a, b, want_all)
         assert np.array_equal(ex, want_all)
+
+
+# --- test_exec.cpp:154-182: execute consumes prepacked hierarchical buffers ---
+@pytest.mark.parametrize("numerics", ["exact", "dmma"])
+def test_prepacked_buffers(numerics):
+    shape = T.Shape(37, 29, 41)
+    bs = T.BlocksizeSet({(1, "m"): 12, (1, "k"): 16, (0, "n"): 6, (0, "m"): 4})
+    hier = H.roomy(1)
+    nest = T.build_plan(T.parse_name("A1C0"), bs, hier, shape)
+    a, b, c = O.fill_uniform(13, [(37, 41), (41, 29), (37, 29)])
+    Ap, Bp, Cp = (T.pack(dev(x), nest, op) for x, op in ((a, "A"), (b, "B"), (c, "C")))
+    caps = [hier.capacity(i) for i in range(hier.size())]
+    if O.have_ref():  # device pack == the reference's pack, bitwise
+        for x, op, got in ((a, "A", Ap), (b, "B", Bp), (c, "C", Cp)):
+            assert np.array_equal(got.cpu().numpy(), O.ref_pack("A1C0", caps, (37, 29, 41), bs.as_dict(), op, x))
+    for x, op, got in ((a, "A", Ap), (b, "B", Bp)):  # round trip
+        assert np.array_equal(T.unpack(got, nest, op).cpu().numpy(), x)
+    T.execute_packed(nest, Ap, Bp, Cp, T.ExecOptions(numerics=numerics))
+    torch.cuda.synchronize()
+    out = T.unpack(Cp, nest, "C").cpu().numpy()
+    want = oracle_exec(nest, a, b, c)
+    if O.have_ref():
+        ref = c.copy()
+        O.ref_execute("A1C0", caps, (37, 29, 41), bs.as_dict(), a, b, ref, packed=True)
+        assert np.array_equal(ref, want)
+    check(numerics, out, a, b, c, nest, want, None)

@@ -74,7 +74,7 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--once", action="store_true")
     ap.add_argument("--schedules", default="fused")
-    ap.add_argument("--tiles", default="128x128,128x64")
+    ap.add_argument("--tiles", default="auto,128x128,128x64")
     ap.add_argument("--only", default="", help="comma-separated config names to run (default: all)")
     ap.add_argument("--members", default="", help="comma-separated family members (default: per config)")
     ap.add_argument("--l2-frac", type=float, default=1.0, help="effective L2 capacity fraction for derivation")
@@ -101,7 +101,7 @@ def main():
             for sched, tile in [(sc, tl) for sc in a.schedules.split(",") for tl in a.tiles.split(",")]:
                 if sched == "faithful" and tile != a.tiles.split(",")[0]:
                     continue
-                tm, tn = (int(x) for x in tile.split("x"))
+                tm, tn = (0, 0) if tile == "auto" else (int(x) for x in tile.split("x"))
                 rec = {"config": cfg, "shape": shape, "family": name, "schedule": sched, "cta_tile": tile,
                        "l2_frac": L2_FRAC}
                 try:
