@@ -361,3 +361,28 @@ def test_prepacked_buffers(numerics):
         O.ref_execute("A1C0", caps, (37, 29, 41), bs.as_dict(), a, b, ref, packed=True)
         assert np.array_equal(ref, want)
     check(numerics, out, a, b, c, nest, want, None)
+
+
+def test_randomized_split_modes_and_tiles():
+    """Odd shapes x every k-split lowering (none / uniform / auto tail /
+    stream-K) x every DMMA tile variant: within the bound, and each
+    configuration bitwise reproducible."""
+    rng = np.random.default_rng(77)
+    hier = T.gpu_hierarchy(128)
+    d = T.parse_name("C2A1C0")
+    for trial in range(10):
+        m, n = (int(x) for x in rng.integers(130, 1400, size=2))
+        k = int(rng.integers(600, 5000))
+        bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(128, 128)),
+                                 pinned=T.BlocksizeSet({(1, "m"): 128}))
+        nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+        a, b, c = O.fill_uniform(500 + trial, [(m, k), (k, n), (m, n)])
+        ii, jj = rng.integers(0, m, 600), rng.integers(0, n, 600)
+        want, ab = O.entries(k, a, m, b, k, c, m, ii, jj)
+        for split in (1, 3, 0, -1):
+            for tile, tile_n in ((0, 0), (128, 128), (128, 64), (64, 64)):
+                kw = dict(split_k=split, tile=tile, tile_n=tile_n)
+                got = run_gpu(nest, a, b, c, **kw)
+                ok, worst = H.entrywise_ok(got[ii + jj * m], want, ab, k, c0=c[ii + jj * m])
+                assert ok, (trial, m, n, k, kw, worst)
+                assert np.array_equal(got, run_gpu(nest, a, b, c, **kw)), (trial, kw)
