@@ -328,7 +328,7 @@ def our_arm(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "FP64 DMMA issue-rate probe run live in this bench (MEASURED_PEAKS.json has no "
                                     "FP64 figure); nominal 148 SM x 64 FMA/clk x 1.965 GHz = 37.2",
-                     "kernel": "k_dmma<BM=128,BN=128,BK=32,WM=64,WN=32,stages=3,vec16>", "algorithmic_flops_per_launch": flops,
+                     "kernel": "k_dmma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3,vec16> (16 warps)", "algorithmic_flops_per_launch": flops,
                      "traffic_source": traffic_src},
         "model": {"hbm_bytes_model": hbm_model_bytes,
                   "hbm_bytes_measured": traffic,

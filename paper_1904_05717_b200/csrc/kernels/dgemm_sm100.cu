@@ -524,8 +524,8 @@ struct Entry {
 };
 
 const Entry kTable[kKernelCount] = {
-    {{(const void*)k_dmma<128, 128, kBKBig, 64, 32, kStagesBig, false>, (const void*)k_dmma<128, 128, kBKBig, 64, 32, kStagesBig, true>},
-     128, 128, 256, dmma_smem<128, 128, kBKBig, kStagesBig>()},
+    {{(const void*)k_dmma<128, 128, kBKBig, 32, 32, kStagesBig, false>, (const void*)k_dmma<128, 128, kBKBig, 32, 32, kStagesBig, true>},
+     128, 128, 512, dmma_smem<128, 128, kBKBig, kStagesBig>()},
     {{(const void*)k_dmma<64, 64, kBKSmall, 32, 32, kStagesSmall, false>, (const void*)k_dmma<64, 64, kBKSmall, 32, 32, kStagesSmall, true>},
      64, 64, 128, dmma_smem<64, 64, kBKSmall, kStagesSmall>()},
     {{(const void*)k_simt<64, 64, 4, 4, kStagesSimt, false>, (const void*)k_simt<64, 64, 4, 4, kStagesSimt, false>},
