@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libtilemul_b200.so")
+# TILEMUL_B200_LIB: load another build of the library (A/B kernel experiments)
+LIB_PATH = os.environ.get("TILEMUL_B200_LIB") or os.path.join(PKG, "lib", "libtilemul_b200.so")
 
 
 class tm_level(C.Structure):

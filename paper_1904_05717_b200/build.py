@@ -27,7 +27,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXFLAGS = ["-std=c++17", "-O2", "-fPIC", "-Wall", "-Wno-unused-function", f"-I{CUDA_HOME}/include",
             f"-I{os.path.join(ROOT, 'include')}"]
 NVFLAGS = ARCH + ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-                  f"-I{os.path.join(ROOT, 'include')}"]
+                  f"-I{os.path.join(ROOT, 'include')}"] + os.environ.get("TILEMUL_B200_NVFLAGS", "").split()
 
 
 def _headers():
