@@ -205,6 +205,42 @@ int tm_fill_uniform_device(double* x, int64_t count, uint64_t seed, uint64_t off
 int tm_fill_uniform_block(double* x, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
                           int64_t col0, int64_t global_ld, void* stream);
 
+/* --- trace-driven model check (include/tilemul/trace.hpp, cachesim.hpp) --- */
+/* Counts of one simulated level; replaces SimLevelStats (cachesim.hpp:18-38).
+ * Operand arrays are indexed A, B, C. */
+typedef struct {
+    int32_t level;
+    int64_t capacity_lines, granularity;
+    int64_t hits, read_misses, write_misses;
+    int64_t fetched_lines, passthrough_writes, writebacks;
+    int64_t per_operand_misses[3], per_operand_writebacks[3];
+} tm_sim_level;
+typedef struct tm_sim tm_sim;
+
+/* trace_event_count (trace.hpp:73-79): 2mn + k(m+n) events per cell. */
+int64_t tm_trace_event_count(const tm_plan* plan);
+/* generate_trace (trace.hpp:51-71): the first `cap` events of the plan's
+ * element-access stream, operand letter / flat index / 1 = write; packed != 0
+ * addresses operands in the plan's prepacked layouts (TraceLayouts::packed),
+ * else column-major. *count = the full stream length. */
+int tm_trace(const tm_plan* plan, int packed, int64_t cap, char* ops, int64_t* indices, uint8_t* writes,
+             int64_t* count);
+/* LruSimulator (cachesim.hpp:61-96): fully associative LRU per level over the
+ * address space of an m x n x k problem (A, then B, then C); level 0 is only
+ * simulated when include_registers != 0. Fails with 2 when the address space
+ * exceeds 2^31 elements (the reference's limit, :71-72). */
+int tm_sim_create(const tm_level* levels, int nlevels, int64_t m, int64_t n, int64_t k, int include_registers,
+                  int flush_dirty_at_end, tm_sim** sim);
+void tm_sim_destroy(tm_sim* sim);
+/* LruSimulator::access (:98-160) for `count` events (ops 'A'/'B'/'C'; writes may be NULL = all reads). */
+int tm_sim_access(tm_sim* sim, const char* ops, const int64_t* indices, const uint8_t* writes, int64_t count);
+/* simulate (:356-362) without the buffer round-trip: replays the plan's trace into sim. */
+int tm_sim_replay(tm_sim* sim, const tm_plan* plan, int packed);
+/* LruSimulator::finish (:162-169): flushes dirty lines when configured; levels innermost first. */
+int tm_sim_finish(tm_sim* sim, tm_sim_level* out, int cap, int* count, int64_t* events);
+/* Lines resident at one simulated level (position innermost first), in slot order (:174-182). */
+int tm_sim_resident_lines(const tm_sim* sim, int position, int64_t* lines, int cap, int* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -106,6 +106,16 @@ def ref():
         L.ref_pack.argtypes = [cp] + hier + bs + [C.c_char, C.c_void_p, C.c_void_p, C.c_char_p, C.c_int]
         L.ref_select.argtypes = [C.c_int64] * 4
         L.ref_select.restype = C.c_char
+        shier = [_i64p, _i64p, _i32p, C.c_int]
+        L.ref_sim_events.argtypes = shier + [C.c_int64] * 3 + [C.c_int, C.c_int, C.c_char_p, _i64p,
+                                                               np.ctypeslib.ndpointer(dtype=np.uint8), C.c_int64,
+                                                               _i64p, C.POINTER(C.c_int), C.POINTER(C.c_int64),
+                                                               C.c_char_p, C.c_int]
+        L.ref_simulate.argtypes = [cp] + hier + bs + shier + [C.c_int, C.c_int, C.c_int, _i64p, C.POINTER(C.c_int),
+                                                              C.POINTER(C.c_int64), C.c_char_p, C.c_int]
+        L.ref_trace.argtypes = [cp] + hier + bs + [C.c_int, C.c_int64, C.c_char_p, _i64p,
+                                                   np.ctypeslib.ndpointer(dtype=np.uint8), C.POINTER(C.c_int64),
+                                                   C.c_char_p, C.c_int]
         _ref = L
     return _ref
 
@@ -270,3 +280,63 @@ def ref_pack(name, caps, shape, bs, op, src, inclusive=None):
     if rc != 0:
         raise ValueError(err.value.decode())
     return dst
+
+
+# --- trace generator / LRU simulator of the reference ----------------------
+SIM_FIELDS = ("level", "capacity_lines", "granularity", "hits", "read_misses", "write_misses", "fetched_lines",
+              "passthrough_writes", "writebacks", "misses_A", "misses_B", "misses_C", "writebacks_A",
+              "writebacks_B", "writebacks_C")
+
+
+def _sim_hier(levels):
+    """levels: [(capacity, granularity, inclusive, write_allocate, write_back)]."""
+    caps = np.array([lv[0] for lv in levels], dtype=np.int64)
+    gran = np.array([lv[1] for lv in levels], dtype=np.int64)
+    flags = np.array([int(bool(x)) for lv in levels for x in lv[2:5]], dtype=np.int32)
+    return caps, gran, flags, len(levels)
+
+
+def _sim_out(rc, out, nout, events, err):
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    return [dict(zip(SIM_FIELDS, map(int, out[15 * i:15 * i + 15]))) for i in range(nout.value)], events.value
+
+
+def ref_sim_events(levels, shape, ops, idx, writes, include_registers=False, flush=True):
+    """The reference LruSimulator over an explicit event list -> ([level stats], events)."""
+    L = ref()
+    out = np.zeros(15 * 16, dtype=np.int64)
+    nout, ev = C.c_int(0), C.c_int64(0)
+    err = C.create_string_buffer(4096)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    wr = np.ascontiguousarray(writes, dtype=np.uint8)
+    rc = L.ref_sim_events(*_sim_hier(levels), *shape, int(include_registers), int(flush), "".join(ops).encode(),
+                          idx, wr, idx.size, out, C.byref(nout), C.byref(ev), err, 4096)
+    return _sim_out(rc, out, nout, ev, err)
+
+
+def ref_simulate(name, caps, shape, bs, sim_levels, packed=False, include_registers=False, flush=True):
+    """The reference simulate() of build_plan(name, caps, shape, bs) through sim_levels."""
+    L = ref()
+    out = np.zeros(15 * 16, dtype=np.int64)
+    nout, ev = C.c_int(0), C.c_int64(0)
+    err = C.create_string_buffer(4096)
+    rc = L.ref_simulate(name.encode(), *_hier_args(caps), *shape, *_bs_args(bs), *_sim_hier(sim_levels),
+                        int(packed), int(include_registers), int(flush), out, C.byref(nout), C.byref(ev), err, 4096)
+    return _sim_out(rc, out, nout, ev, err)
+
+
+def ref_trace(name, caps, shape, bs, packed=False, cap=1 << 20):
+    """The reference generate_trace (first `cap` events) -> (ops str, idx, writes, total count)."""
+    L = ref()
+    ops = C.create_string_buffer(max(1, cap))
+    idx = np.zeros(max(1, cap), dtype=np.int64)
+    wr = np.zeros(max(1, cap), dtype=np.uint8)
+    cnt = C.c_int64(0)
+    err = C.create_string_buffer(4096)
+    rc = L.ref_trace(name.encode(), *_hier_args(caps), *shape, *_bs_args(bs), int(packed), cap, ops, idx, wr,
+                     C.byref(cnt), err, 4096)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    n = min(cap, cnt.value)
+    return ops.raw[:n].decode(), idx[:n], wr[:n], cnt.value

@@ -274,4 +274,88 @@ int ref_pack(const char* name, const int64_t* caps, const int* inclusive, int nl
 
 char ref_select(int64_t m, int64_t n, int64_t k, int64_t cap) { return to_char(select_algorithm(Shape(m, n, k), cap)); }
 
+// --- trace generator and LRU simulator (trace.hpp, cachesim.hpp) ----------
+// Hierarchy with every CacheLevel field: flags[3*i] = inclusive,
+// [3*i+1] = write_allocate, [3*i+2] = write_back.
+static CacheHierarchy make_hier_flags(const int64_t* caps, const int64_t* gran, const int* flags, int nlev) {
+    std::vector<CacheLevel> lv;
+    for (int i = 0; i < nlev; ++i)
+        lv.push_back({i, caps[i], gran[i], flags[3 * i] != 0, flags[3 * i + 1] != 0, flags[3 * i + 2] != 0});
+    return CacheHierarchy(std::move(lv));
+}
+
+// 15 values per simulated level: level, capacity_lines, granularity, hits,
+// read_misses, write_misses, fetched_lines, passthrough_writes, writebacks,
+// per_operand_misses[A,B,C], per_operand_writebacks[A,B,C].
+static void put_stats(const SimResult& r, int64_t* out, int* nout, int64_t* events) {
+    int i = 0;
+    for (const auto& s : r.levels) {
+        int64_t* o = out + 15 * i++;
+        const int64_t v[9] = {s.level, s.capacity_lines, s.granularity, s.hits, s.read_misses, s.write_misses,
+                              s.fetched_lines, s.passthrough_writes, s.writebacks};
+        for (int q = 0; q < 9; ++q) o[q] = v[q];
+        for (int q = 0; q < 3; ++q) {
+            o[9 + q] = s.per_operand_misses[static_cast<std::size_t>(q)];
+            o[12 + q] = s.per_operand_writebacks[static_cast<std::size_t>(q)];
+        }
+    }
+    *nout = i;
+    *events = r.events;
+}
+
+static Operand op_of(char c) { return c == 'A' ? Operand::A : c == 'B' ? Operand::B : Operand::C; }
+
+// LruSimulator over an explicit event list.
+int ref_sim_events(const int64_t* caps, const int64_t* gran, const int* flags, int nlev, int64_t m, int64_t n,
+                   int64_t k, int include_registers, int flush, const char* ops, const int64_t* idx,
+                   const uint8_t* writes, int64_t count, int64_t* out, int* nout, int64_t* events, char* err,
+                   int errlen) {
+    return guarded(err, errlen, [&] {
+        SimOptions o;
+        o.include_registers = include_registers != 0;
+        o.flush_dirty_at_end = flush != 0;
+        LruSimulator sim(make_hier_flags(caps, gran, flags, nlev), Shape(m, n, k), o);
+        for (int64_t e = 0; e < count; ++e)
+            sim.access({op_of(ops[e]), idx[e], writes[e] ? AccessKind::write : AccessKind::read});
+        put_stats(sim.finish(), out, nout, events);
+    });
+}
+
+// simulate(build_plan(name, plan hierarchy, shape, bs), layouts, sim hierarchy).
+int ref_simulate(const char* name, const int64_t* caps, const int* inclusive, int nlev, int64_t m, int64_t n,
+                 int64_t k, const int* bl, const char* bd, const int64_t* bv, int nb, const int64_t* scaps,
+                 const int64_t* sgran, const int* sflags, int snlev, int packed, int include_registers, int flush,
+                 int64_t* out, int* nout, int64_t* events, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        Shape shape(m, n, k);
+        LoopNest nest = build_plan(parse_name(name), make_bs(bl, bd, bv, nb), make_hier(caps, inclusive, nlev), shape);
+        SimOptions o;
+        o.include_registers = include_registers != 0;
+        o.flush_dirty_at_end = flush != 0;
+        const TraceLayouts lay = packed ? TraceLayouts::packed(nest) : TraceLayouts::column_major(shape);
+        put_stats(simulate(nest, lay, make_hier_flags(scaps, sgran, sflags, snlev), o), out, nout, events);
+    });
+}
+
+// The first `cap` events of generate_trace; *count = trace_event_count.
+int ref_trace(const char* name, const int64_t* caps, const int* inclusive, int nlev, int64_t m, int64_t n, int64_t k,
+              const int* bl, const char* bd, const int64_t* bv, int nb, int packed, int64_t cap, char* ops,
+              int64_t* idx, uint8_t* writes, int64_t* count, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        Shape shape(m, n, k);
+        LoopNest nest = build_plan(parse_name(name), make_bs(bl, bd, bv, nb), make_hier(caps, inclusive, nlev), shape);
+        const TraceLayouts lay = packed ? TraceLayouts::packed(nest) : TraceLayouts::column_major(shape);
+        int64_t e = 0;
+        generate_trace(nest, lay, [&](const TraceEvent& t) {
+            if (e < cap) {
+                ops[e] = to_char(t.op);
+                idx[e] = t.index;
+                writes[e] = t.kind == AccessKind::write ? 1 : 0;
+            }
+            ++e;
+        });
+        *count = trace_event_count(nest);
+    });
+}
+
 }  // extern "C"

@@ -40,6 +40,13 @@ class tm_exec_opts(C.Structure):
                 ("tile", C.c_int32), ("tile_n", C.c_int32)]
 
 
+class tm_sim_level(C.Structure):
+    _fields_ = [("level", C.c_int32), ("capacity_lines", C.c_int64), ("granularity", C.c_int64),
+                ("hits", C.c_int64), ("read_misses", C.c_int64), ("write_misses", C.c_int64),
+                ("fetched_lines", C.c_int64), ("passthrough_writes", C.c_int64), ("writebacks", C.c_int64),
+                ("per_operand_misses", C.c_int64 * 3), ("per_operand_writebacks", C.c_int64 * 3)]
+
+
 # (name, restype, argtypes) for every symbol declared in include/tilemul_b200.h
 P = C.c_void_p
 i32, i64, dbl, cstr = C.c_int32, C.c_int64, C.c_double, C.c_char_p
@@ -85,6 +92,14 @@ SIGNATURES = [
     ("tm_measure_fp64_peak", C.c_int, [C.c_int, C.POINTER(dbl)]),
     ("tm_fill_uniform_device", C.c_int, [P, i64, C.c_uint64, C.c_uint64, P]),
     ("tm_fill_uniform_block", C.c_int, [P, i64, i64, i64, C.c_uint64, i64, i64, i64, P]),
+    ("tm_trace_event_count", i64, [P]),
+    ("tm_trace", C.c_int, [P, C.c_int, i64, P, P, P, C.POINTER(i64)]),
+    ("tm_sim_create", C.c_int, [C.POINTER(tm_level), C.c_int, i64, i64, i64, C.c_int, C.c_int, C.POINTER(P)]),
+    ("tm_sim_destroy", None, [P]),
+    ("tm_sim_access", C.c_int, [P, P, P, P, i64]),
+    ("tm_sim_replay", C.c_int, [P, P, C.c_int]),
+    ("tm_sim_finish", C.c_int, [P, C.POINTER(tm_sim_level), C.c_int, C.POINTER(C.c_int), C.POINTER(i64)]),
+    ("tm_sim_resident_lines", C.c_int, [P, C.c_int, C.POINTER(i64), C.c_int, C.POINTER(C.c_int)]),
 ]
 
 _lib = None

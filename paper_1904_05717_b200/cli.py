@@ -1,11 +1,12 @@
 """Command-line surface on the GPU, mirroring the reference CLI's `run`,
-`analyze` and `plan` subcommands (/root/reference/proj/tools/
-tilemul_main.cpp:163-177, :231-304, :306-360): same flags where they apply,
+`analyze`, `simulate` and `plan` subcommands (/root/reference/proj/tools/
+tilemul_main.cpp:163-229, :231-304, :306-360): same flags where they apply,
 same JSON keys, same exit codes — 0 ok, 1 validation/parse/infeasible or a
 failed correctness check, 2 usage/config error (:519-535).
 
     python -m paper_1904_05717_b200 run --alg C2A1C0 --shape 2048 --format json
     python -m paper_1904_05717_b200 analyze --alg C2A1C0 --shape 16384 [--hier gpu.json]
+    python -m paper_1904_05717_b200 simulate --alg B3A2C0 --hier h.json --shape 384 --bs 3:n=192 ...
     python -m paper_1904_05717_b200 plan --shape 65536x256x1024
 
 Differences, by design: the hierarchy defaults to the current B200's
@@ -183,6 +184,59 @@ def cmd_analyze(a) -> int:  # tilemul_main.cpp:163-177 + costmodel.hpp:163-229
     return 0
 
 
+def cmd_simulate(a) -> int:  # tilemul_main.cpp:179-229 + serialize.hpp:174-235
+    d, bs, hier, shape = resolve(a)
+    nest = T.build_plan(d, bs, hier, shape)
+    lay = T.TraceLayouts.column_major(shape) if a.colmajor_trace else T.TraceLayouts.packed(nest)
+    events = T.trace_event_count(nest)
+    if events > a.max_events:
+        raise ConfigError(f"trace of {events} events exceeds --max-events; use a smaller shape")
+    if a.trace_dump:
+        try:
+            out = open(a.trace_dump, "w")
+        except OSError:
+            raise ConfigError(f"cannot write trace to {a.trace_dump}")
+        with out:
+            T.generate_trace(nest, lay, lambda e: T.write_trace_event(out, e))
+    sim = T.simulate(nest, lay, hier, T.SimOptions(include_registers=a.include_registers))
+    rep = T.multilevel_cost(d, bs, hier, shape)
+    cmp = T.compare_model(sim, rep)
+    if a.format == "csv":
+        rows = ["level,hits,misses,writebacks,sim_elements,model_elements,rel_error"]
+        for c in cmp.levels:
+            s = sim.at_level(c.level)
+            rows.append(f"{c.level},{s.hits},{s.misses()},{s.writebacks},{c.sim_elements},{c.model_elements},"
+                        f"{c.rel_error}")
+        emit(a, "\n".join(rows) + "\n")
+    elif a.format == "human":
+        rows = [f"algorithm {T.format_name(d)}, {sim.events} trace events",
+                "level   hits        misses      writebacks  sim elems     model elems   rel error"]
+        for c in cmp.levels:
+            s = sim.at_level(c.level)
+            rows.append(f"  {c.level}   {s.hits}   {s.misses()}   {s.writebacks}   {c.sim_elements}   "
+                        f"{c.model_elements}   {c.rel_error}")
+        emit(a, "\n".join(rows) + "\n")
+    else:
+        model = {"shape": {"m": shape.m, "n": shape.n, "k": shape.k}, "flops": rep.flops,
+                 "boundary_level": rep.boundary_level,
+                 "intensity_flops_per_byte": rep.intensity_flops_per_byte(),
+                 "levels": [{"level": lt.level,
+                             "operands": {o: {"reads": lt.of(o).reads, "writes": lt.of(o).writes} for o in "ABC"},
+                             "total_elements": lt.total_elements(), "total_bytes": lt.total_bytes()}
+                            for lt in rep.levels]}
+        simj = {"events": sim.events,
+                "levels": [{"level": s.level, "capacity_lines": s.capacity_lines, "granularity": s.granularity,
+                            "hits": s.hits, "misses": s.misses(), "read_misses": s.read_misses,
+                            "write_misses": s.write_misses, "writebacks": s.writebacks,
+                            "transferred_elements": s.transferred_elements()} for s in sim.levels]}
+        cmpj = {"max_rel_error": cmp.max_rel_error,
+                "levels": [{"level": c.level, "model_elements": c.model_elements, "sim_elements": c.sim_elements,
+                            "rel_error": c.rel_error} for c in cmp.levels]}
+        emit(a, json.dumps({"algorithm": T.format_name(d), "simulation": simj, "model": model, "comparison": cmpj},
+                           indent=2, default=lambda x: None if x == float("inf") else x) + "\n")
+    return 0
+
+
 def cmd_plan(a) -> int:  # tilemul_main.cpp:306-360, re-targeted (planner.py)
     defaults(a)
     shape = parse_shape(a.shape)
@@ -200,7 +254,7 @@ def cmd_plan(a) -> int:  # tilemul_main.cpp:306-360, re-targeted (planner.py)
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_1904_05717_b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
-    for name in ("run", "analyze", "plan"):
+    for name in ("run", "analyze", "simulate", "plan"):
         p = sub.add_parser(name)
         p.add_argument("--alg")
         p.add_argument("--hier")
@@ -220,9 +274,15 @@ def main(argv=None) -> int:
             p.add_argument("--numerics", default="dmma", choices=["dmma", "fma", "exact"])
             p.add_argument("--schedule", default="fused", choices=["fused", "faithful"])
             p.add_argument("--colmajor", action="store_true", help="accepted; the GPU path is column-major")
+        if name == "simulate":
+            p.add_argument("--trace-dump", dest="trace_dump", help="write the plain-text trace to a file")
+            p.add_argument("--include-registers", dest="include_registers", action="store_true")
+            p.add_argument("--colmajor-trace", dest="colmajor_trace", action="store_true",
+                           help="address the trace in column-major instead of prepacked layout")
+            p.add_argument("--max-events", dest="max_events", type=int, default=4 * 10 ** 9)
     a = ap.parse_args(argv)
     try:
-        return {"run": cmd_run, "analyze": cmd_analyze, "plan": cmd_plan}[a.cmd](a)
+        return {"run": cmd_run, "analyze": cmd_analyze, "simulate": cmd_simulate, "plan": cmd_plan}[a.cmd](a)
     except (T.ValidationFailure, T.ParseError, T.InfeasibleError) as e:
         sys.stderr.write(f"{e}\n")
         return 1

@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/tilemul_b200.h"
+#include "host/cachesim.hpp"
 #include "host/mmm.hpp"
 #include "kernels/gpu.hpp"
 
@@ -953,3 +954,109 @@ int tm_fill_uniform_device(double* x, int64_t count, uint64_t seed, uint64_t off
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------- trace / simulator
+
+struct tm_sim {
+    CacheSim sim;
+};
+
+int64_t tm_trace_event_count(const tm_plan* plan) {
+    int64_t r = -kUsage;
+    guard([&] {
+        if (plan == nullptr) fail_usage("null plan");
+        r = access_count(plan->nest);
+    });
+    return r;
+}
+
+int tm_trace(const tm_plan* plan, int packed, int64_t cap, char* ops, int64_t* indices, uint8_t* writes,
+             int64_t* count) {
+    return guard([&] {
+        if (plan == nullptr) fail_usage("null plan");
+        if (cap > 0 && (ops == nullptr || indices == nullptr || writes == nullptr)) fail_usage("null event buffer");
+        const TraceAddressing lay =
+            packed ? TraceAddressing::packed(plan->nest) : TraceAddressing::column_major(plan->nest.ext);
+        int64_t n = 0;
+        for_each_access(plan->nest, lay, [&](const Access& a) {
+            if (n < cap) {
+                ops[n] = opnd_char(a.op);
+                indices[n] = a.index;
+                writes[n] = a.write ? 1 : 0;
+            }
+            ++n;
+        });
+        if (count) *count = n;
+    });
+}
+
+int tm_sim_create(const tm_level* levels, int nlevels, int64_t m, int64_t n, int64_t k, int include_registers,
+                  int flush_dirty_at_end, tm_sim** sim) {
+    return guard([&] {
+        if (sim == nullptr) fail_usage("null output");
+        *sim = new tm_sim{CacheSim(hierarchy_from(levels, nlevels), make_extents(m, n, k),
+                                   SimConfig{include_registers != 0, flush_dirty_at_end != 0})};
+    });
+}
+
+void tm_sim_destroy(tm_sim* sim) { delete sim; }
+
+int tm_sim_access(tm_sim* sim, const char* ops, const int64_t* indices, const uint8_t* writes, int64_t count) {
+    return guard([&] {
+        if (sim == nullptr) fail_usage("null simulator");
+        if (count > 0 && (ops == nullptr || indices == nullptr)) fail_usage("null event buffer");
+        for (int64_t e = 0; e < count; ++e) {
+            const Opnd op = opnd_of_char(ops[e]);
+            if (indices[e] < 0) fail_usage("negative element index");
+            sim->sim.access(Access{op, indices[e], writes != nullptr && writes[e] != 0});
+        }
+    });
+}
+
+int tm_sim_replay(tm_sim* sim, const tm_plan* plan, int packed) {
+    return guard([&] {
+        if (sim == nullptr || plan == nullptr) fail_usage("null simulator or plan");
+        const TraceAddressing lay =
+            packed ? TraceAddressing::packed(plan->nest) : TraceAddressing::column_major(plan->nest.ext);
+        for_each_access(plan->nest, lay, [&](const Access& a) { sim->sim.access(a); });
+    });
+}
+
+int tm_sim_finish(tm_sim* sim, tm_sim_level* out, int cap, int* count, int64_t* events) {
+    return guard([&] {
+        if (sim == nullptr) fail_usage("null simulator");
+        const auto st = sim->sim.finish();
+        if (count) *count = static_cast<int>(st.size());
+        if (events) *events = sim->sim.events();
+        if (out == nullptr) return;
+        if (static_cast<int>(st.size()) > cap) fail_usage("level buffer too small");
+        for (std::size_t i = 0; i < st.size(); ++i) {
+            const SimStats& s = st[i];
+            tm_sim_level& o = out[i];
+            o.level = s.level;
+            o.capacity_lines = s.capacity_lines;
+            o.granularity = s.granularity;
+            o.hits = s.hits;
+            o.read_misses = s.read_misses;
+            o.write_misses = s.write_misses;
+            o.fetched_lines = s.fetched_lines;
+            o.passthrough_writes = s.passthrough_writes;
+            o.writebacks = s.writebacks;
+            for (int q = 0; q < 3; ++q) {
+                o.per_operand_misses[q] = s.op_misses[static_cast<std::size_t>(q)];
+                o.per_operand_writebacks[q] = s.op_writebacks[static_cast<std::size_t>(q)];
+            }
+        }
+    });
+}
+
+int tm_sim_resident_lines(const tm_sim* sim, int position, int64_t* lines, int cap, int* count) {
+    return guard([&] {
+        if (sim == nullptr) fail_usage("null simulator");
+        const auto r = sim->sim.resident(position);
+        if (count) *count = static_cast<int>(r.size());
+        if (lines == nullptr) return;
+        if (static_cast<int>(r.size()) > cap) fail_usage("line buffer too small");
+        std::copy(r.begin(), r.end(), lines);
+    });
+}

@@ -21,7 +21,9 @@ Blocked make_blocked(i64 rows, i64 cols, std::vector<Cut> cuts) {
 
 // Walk the cuts outermost-first: each cut selects the block containing
 // (i, j) and adds the elements of all blocks before it.
-i64 Blocked::address(i64 i, i64 j) const {
+i64 Blocked::address(i64 i, i64 j) const { return locate(i, j).first; }
+
+std::pair<i64, i64> Blocked::locate(i64 i, i64 j) const {
     if (i < 0 || i >= rows || j < 0 || j >= cols) fail_usage("element index outside matrix");
     i64 base = 0, r0 = 0, r1 = rows, c0 = 0, c1 = cols;
     for (const auto& c : cuts) {
@@ -37,7 +39,7 @@ i64 Blocked::address(i64 i, i64 j) const {
             c1 = std::min(c0 + c.size, c1);
         }
     }
-    return base + (i - r0) + (j - c0) * (r1 - r0);
+    return {base + (i - r0) + (j - c0) * (r1 - r0), r1 - r0};
 }
 
 Blocked layout_of(const Nest& nest, Opnd op) {

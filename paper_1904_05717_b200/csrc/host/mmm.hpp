@@ -230,6 +230,9 @@ struct Blocked {
     std::vector<Cut> cuts;
     bool blocked() const { return !cuts.empty(); }
     i64 address(i64 i, i64 j) const;  // bijection onto [0, rows*cols)
+    // address(i, j) plus the row extent of the column-major leaf block
+    // holding (i, j): inside one leaf, (i+1, j) is +1 and (i, j+1) is +rows.
+    std::pair<i64, i64> locate(i64 i, i64 j) const;
 };
 Blocked make_blocked(i64 rows, i64 cols, std::vector<Cut> cuts);  // same-axis cuts must divide
 Blocked layout_of(const Nest& nest, Opnd op);                      // layout_for

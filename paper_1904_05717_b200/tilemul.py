@@ -715,3 +715,208 @@ def measure_fp64_peak(launches: int = 20) -> float:
     v = C.c_double(0)
     _check(N.lib().tm_measure_fp64_peak(launches, C.byref(v)))
     return v.value
+
+
+# ------------------------------------------- trace-driven model check
+# trace.hpp / cachesim.hpp: the element-access stream of a nest, replayed
+# through a multilevel fully associative LRU hierarchy (native, C ABI
+# tm_trace / tm_sim_*), and the model-vs-simulation comparison.
+READ, WRITE = "R", "W"  # AccessKind::read / write
+
+
+@dataclass(frozen=True)
+class TraceEvent:  # trace.hpp:17-21
+    op: str
+    index: int
+    kind: str  # "R" | "W"
+
+
+@dataclass(frozen=True)
+class TraceLayouts:  # trace.hpp:27-46
+    """Operand addressing of a trace: column-major, or the nest's packed layouts."""
+    a: BlockLayout
+    b: BlockLayout
+    c: BlockLayout
+    packed_layouts: bool = False
+
+    @staticmethod
+    def column_major(s: Shape) -> "TraceLayouts":
+        return TraceLayouts(BlockLayout(s.m, s.k), BlockLayout(s.k, s.n), BlockLayout(s.m, s.n), False)
+
+    @staticmethod
+    def packed(nest: "LoopNest") -> "TraceLayouts":
+        return TraceLayouts(layout_for(nest, "A"), layout_for(nest, "B"), layout_for(nest, "C"), True)
+
+    def of(self, op: str) -> BlockLayout:
+        return {"A": self.a, "B": self.b, "C": self.c}[op]
+
+
+def trace_event_count(nest: "LoopNest") -> int:  # trace.hpp:73-79
+    r = int(N.lib().tm_trace_event_count(nest._ptr))
+    if r < 0:
+        _check(-r)
+    return r
+
+
+def generate_trace(nest: "LoopNest", lay: TraceLayouts, sink=None, limit: Optional[int] = None):
+    """The nest's element accesses in program order (trace.hpp:51-71). Calls
+    sink(event) per event when given, else returns the list. `limit` caps the
+    number of events materialised (the full stream is trace_event_count)."""
+    total = trace_event_count(nest)
+    cap = total if limit is None else min(limit, total)
+    ops = (C.c_char * max(1, cap))()
+    idx = (C.c_int64 * max(1, cap))()
+    wr = (C.c_uint8 * max(1, cap))()
+    cnt = C.c_int64(0)
+    _check(N.lib().tm_trace(nest._ptr, int(lay.packed_layouts), cap, ops, idx, wr, C.byref(cnt)))
+    raw = bytes(ops)[:cap].decode()
+    events = [TraceEvent(raw[e], idx[e], WRITE if wr[e] else READ) for e in range(cap)]
+    if sink is None:
+        return events
+    for e in events:
+        sink(e)
+    return None
+
+
+def write_trace_event(out, e: TraceEvent) -> None:  # trace.hpp:82-84: "OPERAND index R|W"
+    out.write(f"{e.op} {e.index} {e.kind}\n")
+
+
+@dataclass
+class SimLevelStats:  # cachesim.hpp:18-38
+    level: int
+    capacity_lines: int
+    granularity: int
+    hits: int
+    read_misses: int
+    write_misses: int
+    fetched_lines: int
+    passthrough_writes: int
+    writebacks: int
+    per_operand_misses: Dict[str, int]
+    per_operand_writebacks: Dict[str, int]
+
+    def misses(self) -> int:
+        return self.read_misses + self.write_misses
+
+    def transferred_elements(self) -> int:
+        """Elements crossing the boundary above this level, both directions."""
+        return self.granularity * (self.fetched_lines + self.writebacks) + self.passthrough_writes
+
+
+@dataclass
+class SimResult:  # cachesim.hpp:40-50
+    levels: List[SimLevelStats]
+    events: int
+
+    def at_level(self, h: int) -> SimLevelStats:
+        for s in self.levels:
+            if s.level == h:
+                return s
+        raise KeyError("level not simulated")
+
+    def outermost(self) -> SimLevelStats:
+        return self.levels[-1]
+
+
+@dataclass
+class SimOptions:  # cachesim.hpp:52-55
+    include_registers: bool = False
+    flush_dirty_at_end: bool = True
+
+
+class LruSimulator:  # cachesim.hpp:61-354
+    """Fully associative LRU per level, inward-out lookups, inclusive
+    back-invalidation, write-allocate / write-back per level (native)."""
+
+    def __init__(self, hier: CacheHierarchy, shape: Shape, opts: Optional[SimOptions] = None):
+        o = opts or SimOptions()
+        h, nh = hier._c()
+        ptr = C.c_void_p(None)
+        _check(N.lib().tm_sim_create(h, nh, shape.m, shape.n, shape.k, int(o.include_registers),
+                                     int(o.flush_dirty_at_end), C.byref(ptr)))
+        self._ptr = ptr
+        self._nlev = hier.size() - (0 if o.include_registers else 1)
+
+    def __del__(self):
+        p = getattr(self, "_ptr", None)
+        if p is not None and p.value and N is not None and N._lib is not None:
+            N._lib.tm_sim_destroy(p)
+            self._ptr = None
+
+    def access(self, e) -> None:
+        """One event: a TraceEvent or an (op, index, kind) tuple."""
+        op, index, kind = (e.op, e.index, e.kind) if isinstance(e, TraceEvent) else e
+        self.access_many([op], [index], [kind == WRITE])
+
+    def access_many(self, ops: Sequence[str], indices: Sequence[int], writes: Optional[Sequence[bool]] = None) -> None:
+        n = len(indices)
+        o = "".join(ops).encode()
+        if len(o) != n:
+            raise ValueError("ops and indices differ in length")
+        ix = (C.c_int64 * max(1, n))(*indices)
+        wr = (C.c_uint8 * max(1, n))(*([int(bool(w)) for w in writes] if writes is not None else [0] * n))
+        _check(N.lib().tm_sim_access(self._ptr, o, ix, wr, n))
+
+    def replay(self, nest: "LoopNest", lay: TraceLayouts) -> None:
+        _check(N.lib().tm_sim_replay(self._ptr, nest._ptr, int(lay.packed_layouts)))
+
+    def simulated_levels(self) -> int:
+        return self._nlev
+
+    def finish(self) -> SimResult:
+        arr = (N.tm_sim_level * 16)()
+        cnt, ev = C.c_int(0), C.c_int64(0)
+        _check(N.lib().tm_sim_finish(self._ptr, arr, 16, C.byref(cnt), C.byref(ev)))
+        lv = []
+        for i in range(cnt.value):
+            a = arr[i]
+            lv.append(SimLevelStats(a.level, a.capacity_lines, a.granularity, a.hits, a.read_misses, a.write_misses,
+                                    a.fetched_lines, a.passthrough_writes, a.writebacks,
+                                    dict(zip(OPERANDS, list(a.per_operand_misses))),
+                                    dict(zip(OPERANDS, list(a.per_operand_writebacks)))))
+        return SimResult(lv, ev.value)
+
+    def resident_lines(self, position: int) -> List[int]:
+        cnt = C.c_int(0)
+        _check(N.lib().tm_sim_resident_lines(self._ptr, position, None, 0, C.byref(cnt)))
+        buf = (C.c_int64 * max(1, cnt.value))()
+        _check(N.lib().tm_sim_resident_lines(self._ptr, position, buf, cnt.value, C.byref(cnt)))
+        return list(buf[:cnt.value])
+
+
+def simulate(nest: "LoopNest", lay: TraceLayouts, hier: CacheHierarchy,
+             opts: Optional[SimOptions] = None) -> SimResult:  # cachesim.hpp:356-362
+    sim = LruSimulator(hier, nest.shape, opts)
+    sim.replay(nest, lay)
+    return sim.finish()
+
+
+@dataclass
+class LevelComparison:  # cachesim.hpp:367-372
+    level: int
+    model_elements: int
+    sim_elements: int
+    rel_error: float
+
+
+@dataclass
+class ComparisonReport:
+    levels: List[LevelComparison]
+    max_rel_error: float
+
+
+def compare_model(sim: SimResult, model: CostReport) -> ComparisonReport:  # cachesim.hpp:379-392
+    """Per simulated level: the model's reads+writes into that level against
+    the simulated boundary transfers. ValueError on mismatched hierarchies."""
+    out, worst = [], 0.0
+    for s in sim.levels:
+        try:
+            lt = model.at_level(s.level)
+        except KeyError:
+            raise ValueError(f"simulated level {s.level} missing from the model report: mismatched hierarchies")
+        me, se = lt.total_elements(), s.transferred_elements()
+        err = (0.0 if se == 0 else float("inf")) if me == 0 else abs(se - me) / me
+        worst = max(worst, err)
+        out.append(LevelComparison(s.level, me, se, err))
+    return ComparisonReport(out, worst)

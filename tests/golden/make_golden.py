@@ -8,6 +8,8 @@ config1_2048.json — BASELINE config 1: FP64 2048^3, mt19937_64(12345)
   uniform(-1,1) A then B, C = 0, family member C2A1C0 executed by the
   reference's execute() (bitwise equal to reference_gemm here).
   Stores checksums, 4096 sampled entries and their (|A||B|)_ij.
+cachesim_cases.json — reference LruSimulator / simulate / generate_trace
+  outputs (seeded event lists, acceptance and unit nests, random plans).
 host_cases.json — reference outputs of parse_name / derive_blocksizes /
   validate_blocksizes / nest_steps / multilevel_cost on seeded random
   configurations, for the host-library parity tests where _ref is absent.
@@ -101,6 +103,83 @@ def host_cases():
     print("host cases:", len(cases), "derive ok:", sum(c["derive_rc"] == 0 for c in cases))
 
 
+def _roomy_caps(top):
+    return [(1 << 20) * 4 ** h for h in range(top + 1)]
+
+
+def cachesim_cases():
+    """Reference LruSimulator / simulate / generate_trace outputs:
+    * events: seeded random event lists over random hierarchies (regenerated
+      in the test from the seed by helpers.random_sim_case; a checksum guards
+      against generator drift);
+    * plans: the acceptance-suite nests (criteria 2, 4, 5), the desk-scale
+      B3A2C0 and two-level Resident C unit cases, and seeded random plans;
+    * traces: event-stream hashes of seeded random plans, both layouts."""
+    import hashlib
+    sys.path.insert(0, os.path.join(os.path.dirname(HERE)))
+    import helpers as H
+    out = {"events": [], "plans": [], "traces": []}
+    for seed in range(60):
+        c = H.random_sim_case(seed)
+        stats, ev = O.ref_sim_events(c["levels"], c["shape"], c["ops"], c["idx"], c["writes"],
+                                     c["include_registers"], c["flush"])
+        out["events"].append({"seed": seed, "checksum": int(sum((i + 1) * (v + 7) for i, v in enumerate(c["idx"]))),
+                              "stats": stats, "events": ev})
+
+    def plan(label, name, caps, shape, bs, sim_levels, packed=False):
+        case = {"label": label, "name": name, "caps": caps, "shape": list(shape),
+                "bs": [[l, d, v] for (l, d), v in sorted(bs.items())], "sim_levels": sim_levels, "packed": packed}
+        try:
+            case["stats"], case["events"] = O.ref_simulate(name, caps, shape, bs, sim_levels, packed=packed)
+        except ValueError as e:  # e.g. packed layouts whose same-axis steps do not divide
+            case["error"] = str(e)
+        out["plans"].append(case)
+
+    for lbl, name, shape, bs, reg in [
+            ("criterion2_resident_C", "C0", (96, 96, 768), {(0, "m"): 96, (0, "n"): 96}, 9216),
+            ("criterion2_resident_A", "A1C0", (96, 768, 96), {(1, "m"): 96, (1, "k"): 96, (0, "n"): 1, (0, "m"): 96}, 128),
+            ("criterion2_resident_B", "B1C0", (768, 96, 96), {(1, "k"): 96, (1, "n"): 96, (0, "m"): 1, (0, "n"): 96}, 128)]:
+        caps = [reg, 10240]
+        plan(lbl, name, caps, shape, bs, [(reg, 1, False, True, True), (10240, 1, False, False, True)])
+    plan("criterion4_right_resident", "C0", [4096, 8192], (64, 64, 1024), {(0, "m"): 64, (0, "n"): 64},
+         [(1, 1, False, True, True), (4096, 1, False, False, True)])
+    c5 = [(64, 1, False, True, True), (2048, 1, False, False, True), (49152, 1, False, False, True)]
+    plan("criterion5_b_outer", "B2A1C0", [64, 2048, 49152], (816, 816, 816),
+         {(2, "n"): 204, (2, "k"): 192, (1, "m"): 24, (1, "k"): 48, (0, "n"): 12, (0, "m"): 4}, c5, packed=True)
+    plan("criterion5_goto", "A1C0", [64, 2048, 49152], (816, 816, 816),
+         {(1, "m"): 24, (1, "k"): 48, (0, "n"): 12, (0, "m"): 4, (2, "n"): 660}, c5, packed=True)
+    desk = [(16, 1, False, True, True), (512, 1, False, False, True), (2048, 1, False, False, True),
+            (49152, 1, False, False, True)]
+    plan("unit_desk_scale_B3A2C0", "B3A2C0", [16, 512, 2048, 49152], (384, 384, 384),
+         {(3, "n"): 192, (3, "k"): 192, (2, "m"): 24, (2, "k"): 48, (0, "n"): 6, (0, "m"): 2}, desk, packed=True)
+    plan("unit_two_level_resident_C", "C0", [2304, 2560], (48, 48, 384), {(0, "m"): 48, (0, "n"): 48},
+         [(2304, 1, False, True, True), (2560, 1, False, False, True)])
+    for seed in range(40):
+        p = H.random_sim_plan(1000 + seed)
+        bs = {(l, d): v for l, d, v in p["bs"]}
+        plan(f"random_{1000 + seed}", p["name"], _roomy_caps(p["top"]), p["shape"], bs, p["sim_levels"],
+             packed=p["packed"])
+    for seed in range(12):
+        p = H.random_sim_plan(2000 + seed)
+        bs = {(l, d): v for l, d, v in p["bs"]}
+        for packed in (False, True):
+            try:
+                ops, idx, wr, n = O.ref_trace(p["name"], _roomy_caps(p["top"]), p["shape"], bs, packed=packed)
+            except ValueError as e:
+                out["traces"].append({"seed": 2000 + seed, "packed": packed, "error": str(e)})
+                continue
+            h = hashlib.sha256(ops.encode() + idx.astype("<i8").tobytes() + wr.tobytes()).hexdigest()
+            out["traces"].append({"seed": 2000 + seed, "packed": packed, "count": n, "sha256": h,
+                                  "head": [[ops[i], int(idx[i]), int(wr[i])] for i in range(min(24, len(ops)))]})
+    json.dump(out, open(os.path.join(HERE, "cachesim_cases.json"), "w"))
+    print("cachesim:", len(out["events"]), "event cases,", len(out["plans"]), "plans,", len(out["traces"]), "traces")
+
+
 if __name__ == "__main__":
-    host_cases()
-    config1()
+    which = sys.argv[1:] or ["host", "config1", "cachesim"]
+    if "host" in which:
+        host_cases()
+    if "config1" in which:
+        config1()
+    if "cachesim" in which:
+        cachesim_cases()

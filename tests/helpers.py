@@ -55,3 +55,51 @@ def entrywise_ok(got, want, absprod, k: int, c0=None, u: float = U64):
     ok = err <= bound
     worst = float(np.max(err / np.where(bound > 0, bound, 1.0))) if err.size else 0.0
     return bool(np.all(ok)), worst
+
+
+def random_sim_case(seed: int):
+    """A seeded random simulator configuration and event list (cachesim
+    golden fixtures, tests/golden/make_golden.py): 1-4 simulated levels with
+    random line sizes and inclusive / write-allocate / write-back flags, and
+    a mixed read/write stream over all three operands."""
+    rng = np.random.default_rng(seed)
+    include_registers = bool(rng.integers(0, 4) == 0)
+    nsim = int(rng.integers(1, 5))
+    levels = [(int(rng.integers(1, 4)), 1, False, True, True)]  # registers
+    cap = levels[0][0]
+    for _ in range(nsim):
+        cap = cap + int(rng.integers(2, 40)) * (1 if rng.integers(0, 2) else 4)
+        gran = int(rng.choice([1, 1, 2, 4]))
+        levels.append((cap, gran, bool(rng.integers(0, 2)), bool(rng.integers(0, 3) > 0), bool(rng.integers(0, 4) > 0)))
+    if include_registers:
+        levels[0] = (levels[0][0], 1, False, bool(rng.integers(0, 2)), bool(rng.integers(0, 2)))
+    shape = tuple(int(x) for x in rng.integers(2, 12, size=3))
+    sizes = {"A": shape[0] * shape[2], "B": shape[2] * shape[1], "C": shape[0] * shape[1]}
+    n = int(rng.integers(200, 1500))
+    ops = [("A", "B", "C")[int(x)] for x in rng.integers(0, 3, size=n)]
+    # skewed indices so reuse happens at every capacity
+    idx = [int(min(sizes[o] - 1, abs(rng.normal(0, sizes[o] / 3)))) for o in ops]
+    writes = [bool(x) for x in (rng.integers(0, 5, size=n) == 0)]
+    flush = bool(rng.integers(0, 5) > 0)
+    return {"levels": levels, "shape": shape, "ops": ops, "idx": idx, "writes": writes,
+            "include_registers": include_registers, "flush": flush}
+
+
+def random_sim_plan(seed: int):
+    """A seeded random (plan, simulated hierarchy) pair for the cachesim
+    golden fixtures: any C-register family member up to 3 levels, random
+    blocksizes on a roomy plan hierarchy, a random simulated hierarchy."""
+    rng = np.random.default_rng(seed)
+    d = random_descriptor(rng)
+    shape = T.Shape(*(int(x) for x in rng.integers(2, 24, size=3)))
+    bs = random_blocksizes(rng, d, shape)
+    nsim = int(rng.integers(1, 4))
+    levels = [(int(rng.integers(1, 9)), 1, False, True, True)]
+    cap = levels[0][0]
+    for _ in range(nsim):
+        cap = cap + int(rng.integers(8, 300))
+        levels.append((cap, int(rng.choice([1, 1, 2, 4, 8])), bool(rng.integers(0, 2)), bool(rng.integers(0, 3) > 0),
+                       bool(rng.integers(0, 4) > 0)))
+    return {"name": T.format_name(d), "top": d.top_level(), "shape": (shape.m, shape.n, shape.k),
+            "bs": [[l, dim, v] for (l, dim), v in bs.entries()], "sim_levels": levels,
+            "packed": bool(rng.integers(0, 2))}

@@ -59,3 +59,43 @@ def test_plan_on_gpu_hierarchy_file():
     assert j["reference_select_algorithm"] == "C"
     ranked = [r["algorithm"] for r in j["ranking"] if r["model_bytes_into_L2"] is not None]
     assert ranked[0] == "B2A1C0"
+
+
+DESK = ["--alg", "B3A2C0", "--shape", "96", "--bs", "3:n=48", "--bs", "3:k=48", "--bs", "2:m=24", "--bs", "2:k=24",
+        "--bs", "0:n=6", "--bs", "0:m=2"]
+
+
+def _desk_hier(tmp_path):
+    p = tmp_path / "desk.json"
+    json.dump({"levels": [{"index": 0, "capacity_elements": 16},
+                          {"index": 1, "capacity_elements": 512, "write_allocate": False},
+                          {"index": 2, "capacity_elements": 2048, "write_allocate": False},
+                          {"index": 3, "capacity_elements": 49152, "write_allocate": False}]}, open(p, "w"))
+    return str(p)
+
+
+def test_simulate_json_csv_and_trace_dump(tmp_path):  # tilemul_main.cpp:179-229
+    h = _desk_hier(tmp_path)
+    rc, out, _ = cli(["simulate", "--hier", h, "--format", "json"] + DESK)
+    assert rc == 0
+    j = json.loads(out)
+    assert j["algorithm"] == "B3A2C0" and set(j) == {"algorithm", "simulation", "model", "comparison"}
+    assert j["simulation"]["events"] == 663552
+    assert [lv["level"] for lv in j["simulation"]["levels"]] == [1, 2, 3]  # registers not simulated by default
+    # the inner levels follow the model exactly at this scale
+    assert [c["rel_error"] for c in j["comparison"]["levels"]][:2] == [0.0, 0.0]
+    rc, out, _ = cli(["simulate", "--hier", h, "--format", "csv", "--include-registers"] + DESK)
+    assert rc == 0
+    rows = out.strip().splitlines()
+    assert rows[0] == "level,hits,misses,writebacks,sim_elements,model_elements,rel_error"
+    assert [r.split(",")[0] for r in rows[1:]] == ["0", "1", "2", "3"]
+    dump = tmp_path / "trace.txt"
+    rc, _, _ = cli(["simulate", "--hier", h, "--trace-dump", str(dump), "--colmajor-trace"] + DESK)
+    assert rc == 0
+    lines = open(dump).read().splitlines()
+    assert len(lines) == 663552 and lines[0] == "C 0 R" and lines[-1].endswith(" W")
+
+
+def test_simulate_refuses_long_traces(tmp_path):
+    rc, _, err = cli(["simulate", "--hier", _desk_hier(tmp_path), "--max-events", "1000"] + DESK)
+    assert rc == 2 and "--max-events" in err
