@@ -108,6 +108,7 @@ struct Schedule {
     bool blocked = false;
     int grid_fixed = 0;
     int regions = 0;         // progress counters (faithful)
+    int counters = 0;        // split-k fix-up counters (DMMA kernels), self-resetting
     std::vector<gpu::Task> host_tasks;
     gpu::Task* tasks = nullptr;
     int32_t* progress = nullptr;
@@ -203,6 +204,19 @@ void check_i32(i64 v, const char* what) {
     if (v > INT32_MAX) fail_usage(std::string(what) + " exceeds the 32-bit task range");
 }
 
+// Workspace slots and self-resetting counters of the in-kernel fix-up.
+void alloc_fixup(Schedule& s, const gpu::KernelInfo& info, int32_t slots, int32_t counters, cudaStream_t stream) {
+    if (counters == 0) return;
+    s.work_ld = info.tile_m;
+    s.work_slice = static_cast<i64>(info.tile_m) * info.tile_n;
+    cuda_check(cudaMalloc(&s.work, sizeof(double) * static_cast<std::size_t>(s.work_slice) * slots),
+               "cudaMalloc(split-k workspace)");
+    cuda_check(cudaMalloc(&s.progress, sizeof(int32_t) * static_cast<std::size_t>(counters)), "cudaMalloc(fix-up counters)");
+    cuda_check(cudaMemsetAsync(s.progress, 0, sizeof(int32_t) * static_cast<std::size_t>(counters), stream),
+               "zero fix-up counters");
+    s.counters = counters;
+}
+
 std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, cudaStream_t stream) {
     auto s = std::make_unique<Schedule>();
     s->kernel = kernel;
@@ -257,16 +271,26 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
                     u = end;
                 }
             }
-            std::vector<int32_t> slot0(tiles.size(), -1);
+            // A cut tile is finished inside the kernel: its head piece (k from
+            // 0, from C) is the owner and runs last in its CTA's range; the
+            // later pieces run first in the following CTAs' ranges and leave
+            // partials in slots slot0 .. slot0+pieces-2 (Task::fixup).
+            // Kernels built without the fix-up keep one slot per piece and a
+            // fixed-order reduce launch afterwards.
+            const bool fixk = kernel == gpu::kDmma128 || kernel == gpu::kDmma64;
+            std::vector<int32_t> slot0(tiles.size(), -1), counter(tiles.size(), -1);
             std::vector<gpu::ReduceTile> red;
-            int32_t next_slot = 0;
+            int32_t next_slot = 0, ncounters = 0;
             for (std::size_t t = 0; t < tiles.size(); ++t)
                 if (pieces[t].size() > 1) {
+                    const int32_t np = static_cast<int32_t>(pieces[t].size());
                     slot0[t] = next_slot;
-                    red.push_back(gpu::ReduceTile{static_cast<int32_t>(tiles[t][0]), static_cast<int32_t>(tiles[t][2]),
-                                                  static_cast<int32_t>(tiles[t][1]), static_cast<int32_t>(tiles[t][3]),
-                                                  next_slot, static_cast<int32_t>(pieces[t].size())});
-                    next_slot += static_cast<int32_t>(pieces[t].size());
+                    counter[t] = ncounters++;
+                    if (!fixk)
+                        red.push_back(gpu::ReduceTile{static_cast<int32_t>(tiles[t][0]), static_cast<int32_t>(tiles[t][2]),
+                                                      static_cast<int32_t>(tiles[t][1]), static_cast<int32_t>(tiles[t][3]),
+                                                      next_slot, np});
+                    next_slot += fixk ? np - 1 : np;
                 }
             std::vector<int32_t> first(static_cast<std::size_t>(G) + 1, 0);
             for (int c = 0; c < G; ++c) {
@@ -281,23 +305,42 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
                     tk.n = static_cast<int32_t>(t[3]);
                     tk.p0 = static_cast<int32_t>(pr[0] * slab);
                     tk.k = static_cast<int32_t>(std::min(pr[1] * slab, e.k) - pr[0] * slab);
-                    tk.tile = -1;
-                    tk.seq = 0;
                     const int32_t s0 = slot0[static_cast<std::size_t>(tile)];
-                    tk.slice = s0 < 0 ? -1 : s0 + static_cast<int32_t>(pi);
+                    const int32_t np = static_cast<int32_t>(pieces[static_cast<std::size_t>(tile)].size());
+                    tk.tile = s0 < 0 ? -1 : counter[static_cast<std::size_t>(tile)];
                     tk.from_c = pr[0] == 0 ? 1 : 0;
+                    if (s0 < 0) {
+                        tk.seq = 0;
+                        tk.slice = -1;
+                        tk.fixup = 0;
+                    } else if (!fixk) {  // every piece into its slot; the reduce launch sums them
+                        tk.tile = -1;
+                        tk.seq = 0;
+                        tk.slice = s0 + static_cast<int32_t>(pi);
+                        tk.fixup = 0;
+                    } else if (pi == 0) {  // owner
+                        tk.seq = np - 1;
+                        tk.slice = s0;
+                        tk.fixup = 2;
+                    } else {
+                        tk.seq = 0;
+                        tk.slice = s0 + static_cast<int32_t>(pi) - 1;
+                        tk.fixup = 1;
+                    }
                     T.push_back(tk);
                 }
             }
             first[static_cast<std::size_t>(G)] = static_cast<int32_t>(T.size());
-            s->slices = static_cast<int>(red.size());
             s->blocked = true;
             s->grid_fixed = G;
             cuda_check(cudaMalloc(&s->cta_first, sizeof(int32_t) * first.size()), "cudaMalloc(cta ranges)");
             cuda_check(cudaMemcpyAsync(s->cta_first, first.data(), sizeof(int32_t) * first.size(),
                                        cudaMemcpyHostToDevice, stream),
                        "upload cta ranges");
-            if (!red.empty()) {
+            if (fixk) {
+                alloc_fixup(*s, info, next_slot, ncounters, stream);
+            } else if (!red.empty()) {
+                s->slices = static_cast<int>(red.size());
                 s->work_ld = info.tile_m;
                 s->work_slice = static_cast<i64>(info.tile_m) * info.tile_n;
                 cuda_check(cudaMalloc(&s->work, sizeof(double) * static_cast<std::size_t>(s->work_slice) * next_slot),
@@ -343,7 +386,13 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
                 for (i64 i = full; i < nt; ++i) parts[static_cast<std::size_t>(i)] = bestS;
             }
         }
-        int32_t next_slot = 0;
+        // DMMA kernels finish split tiles in-kernel (Task::fixup): the owner
+        // part (k from 0, from C) is listed after its contributors, so every
+        // wait points at an earlier task of the persistent grid (no cycle).
+        // (the 128x64 short-k kernel is built without the fix-up: its register
+        // budget is two CTAs per SM; its few tail splits use the reduce launch)
+        const bool fix = kernel == gpu::kDmma128 || kernel == gpu::kDmma64;
+        int32_t next_slot = 0, ncounters = 0;
         std::vector<gpu::ReduceTile> red;
         for (std::size_t ti = 0; ti < tiles.size(); ++ti) {
             const auto& t = tiles[ti];
@@ -364,6 +413,23 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
                 T.push_back(tk);
                 continue;
             }
+            if (fix) {
+                const int32_t ctr = ncounters++;
+                for (int q = 1; q <= used; ++q) {
+                    const int part = q % used;  // contributors 1..used-1, then the owner (part 0)
+                    const i64 p0 = part * per;
+                    tk.p0 = static_cast<int32_t>(p0);
+                    tk.k = static_cast<int32_t>(std::min(per, e.k - p0));
+                    tk.tile = ctr;
+                    tk.from_c = part == 0 ? 1 : 0;
+                    tk.fixup = part == 0 ? 2 : 1;
+                    tk.seq = part == 0 ? used - 1 : 0;
+                    tk.slice = part == 0 ? next_slot : next_slot + part - 1;
+                    T.push_back(tk);
+                }
+                next_slot += used - 1;
+                continue;
+            }
             red.push_back(gpu::ReduceTile{tk.i0, tk.j0, tk.m, tk.n, next_slot, used});
             for (int q = 0; q < used; ++q) {
                 const i64 p0 = q * per;
@@ -375,6 +441,7 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
             }
             next_slot += used;
         }
+        if (fix) alloc_fixup(*s, info, next_slot, ncounters, stream);
         s->slices = static_cast<int>(red.size());
         if (!red.empty()) {
             s->work_ld = info.tile_m;

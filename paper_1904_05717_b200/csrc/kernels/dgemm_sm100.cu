@@ -72,6 +72,46 @@ __device__ __forceinline__ void signal_done(const Args& a, const Task& t) {
     }
 }
 
+// Split-k fix-up inside the task kernel (Task::fixup). Contributors publish
+// their partial with a release increment of the tile's counter; the owner
+// acquires the count, then adds the partials in slot order -- the same sums
+// in the same order as k_reduce_tiles, one launch and one C round trip less.
+__device__ __forceinline__ void signal_partial(const Args& a, const Task& t) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.progress + t.tile) : "memory");
+    }
+}
+
+template <int FM, int FN>
+__device__ __forceinline__ void fold_partials(const Args& a, const Task& t, double (&acc)[FM][FN][2], int wm0,
+                                              int wn0, int g, int tq) {
+    if (threadIdx.x == 0) {
+        int v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(a.progress + t.tile) : "memory");
+            if (v >= t.seq) break;
+            __nanosleep(64);
+        }
+        a.progress[t.tile] = 0;  // every contribution is in: ready for the next launch
+    }
+    __syncthreads();
+    for (int q = 0; q < t.seq; ++q) {
+        const double* w = a.work + static_cast<int64_t>(t.slice + q) * a.work_slice;
+#pragma unroll
+        for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni) {
+                const int r = wm0 + mi * 8 + 2 * tq, c = wn0 + ni * 8 + g;
+                // slots are tile-shaped (work_ld = tile rows, even) and 16-byte aligned
+                const double2 v = __ldcg(reinterpret_cast<const double2*>(w + r + static_cast<int64_t>(c) * a.work_ld));
+                acc[mi][ni][0] = __dadd_rn(acc[mi][ni][0], v.x);
+                acc[mi][ni][1] = __dadd_rn(acc[mi][ni][1], v.y);
+            }
+    }
+}
+
 // Where a task reads its starting value and writes its result.
 struct Dest {
     const double* src;  // nullptr: start from zero
@@ -81,7 +121,14 @@ struct Dest {
 };
 __device__ __forceinline__ Dest resolve(const Args& a, const Task& t) {
     Dest d;
-    if (t.slice < 0) {
+    if (t.fixup == 1) {  // contributor: partial from zero into its slot
+        d.src = nullptr;
+        d.ld_src = a.ldc;
+        d.dst = a.work + static_cast<int64_t>(t.slice) * a.work_slice;
+        d.ld_dst = a.work_ld;
+        d.oi = 0;
+        d.oj = 0;
+    } else if (t.slice < 0 || t.fixup == 2) {
         d.src = a.C;
         d.dst = a.C;
         d.ld_src = d.ld_dst = a.ldc;
@@ -256,7 +303,8 @@ struct Stager {
     }
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V16>
+// FIX: compile the in-kernel split-k fix-up (Task::fixup) into this variant.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool V16, bool FIX = true>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) {
     constexpr int NWM = BM / WM, NT = (BM / WM) * (BN / WN) * 32;
     constexpr int FM = WM / 8, FN = WN / 8, KK = BK / 4;
@@ -351,6 +399,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
         }
         cp_wait<0>();
         __syncthreads();
+        if constexpr (FIX) {
+            if (t.fixup == 2) fold_partials<FM, FN>(a, t, acc, wm0, wn0, g, tq);
+        }
 
         const int64_t di = d.oi, dj = d.oj;
         const bool dst_vec = ((reinterpret_cast<uintptr_t>(d.dst) & 15) | (d.ld_dst & 1) | (di & 1)) == 0;
@@ -368,7 +419,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
                         if (r + e < t.m && c < t.n) p[e] = acc[mi][ni][e];
                 }
             }
-        signal_done(a, t);
+        if (FIX && t.fixup == 1) signal_partial(a, t);
+        else signal_done(a, t);
     }
 }
 
@@ -537,7 +589,7 @@ const Entry kTable[kKernelCount] = {
      64, 64, 256, smem_of<64, 64, true, kStagesSimt>()},
     {{(const void*)k_simt<128, 128, 8, 8, kStagesSimt, false>, (const void*)k_simt<128, 128, 8, 8, kStagesSimt, false>},
      128, 128, 256, smem_of<128, 128, true, kStagesSimt>()},
-    {{(const void*)k_dmma<128, 64, kBKSmall, 64, 32, kStagesRankK, false>, (const void*)k_dmma<128, 64, kBKSmall, 64, 32, kStagesRankK, true>},
+    {{(const void*)k_dmma<128, 64, kBKSmall, 64, 32, kStagesRankK, false, false>, (const void*)k_dmma<128, 64, kBKSmall, 64, 32, kStagesRankK, true, false>},
      128, 64, 128, dmma_smem<128, 64, kBKSmall, kStagesRankK>()},
 };
 

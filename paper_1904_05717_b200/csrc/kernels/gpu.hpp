@@ -20,6 +20,14 @@ struct Task {
     int32_t seq;    // chunks of this region that must finish first
     int32_t slice;  // -1: read/write C; s >= 0: split-k partial into workspace slice s
     int32_t from_c; // slice tasks: 1 = start from C's value, 0 = start from zero
+    // In-kernel split-k fix-up (DMMA kernels; replaces the reduce launch):
+    //   0 — none (slice semantics above);
+    //   1 — contributor: the part's partial goes to workspace slot `slice`,
+    //       then counter `tile` is incremented (release);
+    //   2 — owner (the part that starts from C): after its k loop it waits
+    //       until counter `tile` reaches `seq`, adds slots slice .. slice+seq-1
+    //       in slot order, writes C and resets the counter to 0.
+    int32_t fixup;
 };
 
 struct Args {

@@ -319,7 +319,7 @@ def test_split_k_tail_and_uniform(split):
     a, b, c = O.fill_uniform(41, [(m, k), (k, n), (m, n)])
     got1 = run_gpu(nest, a, b, c, split_k=split)
     launch = nest.last_launch()
-    assert launch["launches"] == 2  # task kernel + tile reduction
+    assert launch["launches"] == 1  # cut tiles are finished in-kernel (Task::fixup), no reduce launch
     assert launch["tasks"] > 256
     got2 = run_gpu(nest, a, b, c, split_k=split)
     assert np.array_equal(got1, got2)
@@ -328,6 +328,13 @@ def test_split_k_tail_and_uniform(split):
     want, ab = O.entries(k, a, m, b, k, c, m, ii, jj)
     ok, worst = H.entrywise_ok(got1[ii + jj * m], want, ab, k, c0=c[ii + jj * m])
     assert ok, worst
+    # the SIMT kernels keep the separate fixed-order reduction launch
+    if split == 3:
+        f1 = run_gpu(nest, a, b, c, numerics="fma", split_k=3)
+        assert nest.last_launch()["launches"] == 2
+        assert np.array_equal(f1, run_gpu(nest, a, b, c, numerics="fma", split_k=3))
+        ok, worst = H.entrywise_ok(f1[ii + jj * m], want, ab, k, c0=c[ii + jj * m])
+        assert ok, worst
     # exact numerics ignore auto-splitting and stay bitwise equal to the reference
     if split == 0:
         ex = run_gpu(nest, a, b, c, numerics="exact", split_k=0)
