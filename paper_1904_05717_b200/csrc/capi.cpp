@@ -16,6 +16,7 @@
 // Either way every C entry is accumulated in ascending k from its incoming
 // value, which is what makes the result independent of the schedule.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -769,20 +770,65 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
             cuda_check(cudaStreamSynchronize(st), "execute_host sync");
             return;
         }
-        // Two-level copy/compute pipeline: C column blocks outer, k-chunks
-        // inner. Block b's C goes up just ahead of its GEMMs and comes back on
-        // a third stream while block b+1 computes; A streams in k-chunks
-        // during block 0, B in (k-chunk, column-block) pieces. Every C entry
-        // still sees its k chunks in ascending order (chunks are multiples of
-        // the 32-deep slab), i.e. exactly the unpipelined operation sequence.
+        // Copy/compute pipeline over (C column block b, k-chunk q) units in
+        // wavefront order (b + q ascending): uploads are issued on one copy
+        // stream in the order the GEMMs first need them (C_b, A_q, B_qb), so
+        // the data the first GEMMs wait for grows with the work they do
+        // instead of all of A arriving during column block 0; a finished
+        // block goes back on a third stream while the rest computes. Every C
+        // entry still sees its k chunks in ascending order (chunks are
+        // multiples of the 32-deep slab), i.e. exactly the unpipelined
+        // operation sequence.
         mkstream(plan->copy_stream);
         mkstream(plan->d2h_stream);
-        const int nq0 = e.k >= 4096 ? static_cast<int>(std::min<i64>(8, e.k / 2048)) : 1;
+        int nq0 = e.k >= 4096 ? static_cast<int>(std::min<i64>(8, e.k / 2048)) : 1;
+        int nb0 = e.n >= 2048 ? static_cast<int>(std::min<i64>(8, e.n / 1024)) : 1;
+        if (const char* v = std::getenv("TM_PIPE_NQ")) nq0 = std::max(1, std::atoi(v));
+        if (const char* v = std::getenv("TM_PIPE_NB")) nb0 = std::max(1, std::atoi(v));
+        const bool taper = std::getenv("TM_PIPE_TAPER") ? std::atoi(std::getenv("TM_PIPE_TAPER")) != 0 : true;
+        const bool wavefront = std::getenv("TM_PIPE_WAVE") ? std::atoi(std::getenv("TM_PIPE_WAVE")) != 0 : true;
         const i64 kc = cdiv(cdiv(e.k, nq0), 32) * 32;
-        const int nq = static_cast<int>(cdiv(e.k, kc));
-        const int nb0 = e.n >= 2048 ? static_cast<int>(std::min<i64>(8, e.n / 1024)) : 1;
         const i64 wb = cdiv(cdiv(e.n, nb0), 128) * 128;
-        const int nbk = static_cast<int>(cdiv(e.n, wb));
+        // Tapered pieces: the first k-chunks and the first and last column
+        // blocks are 1/4 and 1/2 of the regular size, so the copies the first
+        // GEMM waits for, and the last block's download, are small.
+        auto cuts = [](i64 total, i64 base, i64 align, bool taper_end) {
+            std::vector<i64> sz;
+            const i64 q4 = std::max(align, base / 4 / align * align), q2 = std::max(align, base / 2 / align * align);
+            std::vector<i64> head{q4, q2}, tail;
+            if (taper_end) tail = {q2, q4};
+            i64 left = total;
+            for (i64 h : head)
+                if (left > h + base) {
+                    sz.push_back(h);
+                    left -= h;
+                }
+            std::vector<i64> end;
+            for (i64 t : tail)
+                if (left > t + base) {
+                    end.insert(end.begin(), t);
+                    left -= t;
+                }
+            const i64 nmid = cdiv(left, base), each = cdiv(cdiv(left, nmid), align) * align;
+            while (left > 0) {  // the middle in equal aligned pieces (no sliver)
+                const i64 x = std::min(each, left);
+                sz.push_back(x);
+                left -= x;
+            }
+            sz.insert(sz.end(), end.begin(), end.end());
+            std::vector<i64> start{0};
+            for (i64 x : sz) start.push_back(start.back() + x);
+            return start;  // piece i = [start[i], start[i+1])
+        };
+        auto plain = [](i64 total, i64 base) {
+            std::vector<i64> st{0};
+            while (st.back() < total) st.push_back(std::min(total, st.back() + base));
+            return st;
+        };
+        const std::vector<i64> kcut = nq0 > 1 ? (taper ? cuts(e.k, kc, 32, false) : plain(e.k, kc)) : std::vector<i64>{0, e.k};
+        const std::vector<i64> ncut = nb0 > 1 ? (taper ? cuts(e.n, wb, 128, true) : plain(e.n, wb)) : std::vector<i64>{0, e.n};
+        const int nq = static_cast<int>(kcut.size()) - 1;
+        const int nbk = static_cast<int>(ncut.size()) - 1;
         const std::size_t nev = static_cast<std::size_t>(nq + 2 * nbk + nbk * nq);
         while (plan->chunk_ready.size() < nev) {
             cudaEvent_t ev;
@@ -809,21 +855,34 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
         int64_t tasks = 0;
         int32_t launches = 0, ctas = 0;
         auto d2h = [&](int b) {
-            const i64 j0 = b * wb, w = std::min(wb, e.n - j0);
+            const i64 j0 = ncut[static_cast<std::size_t>(b)], w = ncut[static_cast<std::size_t>(b) + 1] - j0;
             cuda_check(cudaStreamWaitEvent(ds, evDone[b], 0), "wait block");
             cuda_check(cudaMemcpyAsync(C + j0 * e.m, plan->dC + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
                                        cudaMemcpyDeviceToHost, ds),
                        "D2H C block");
         };
-        for (int b = 0; b < nbk; ++b) {
-            const i64 j0 = b * wb, w = std::min(wb, e.n - j0);
-            cuda_check(cudaMemcpyAsync(plan->dC + j0 * e.m, C + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
-                                       cudaMemcpyHostToDevice, cs),
-                       "H2D C block");
-            cuda_check(cudaEventRecord(evC[b], cs), "event");
-            for (int q = 0; q < nq; ++q) {
-                const i64 p0 = q * kc, kq = std::min(kc, e.k - p0);
-                if (b == 0) {
+        std::vector<char> have_a(static_cast<std::size_t>(nq), 0);
+        std::vector<int> finished;  // blocks whose D2H is issued one unit later (a pageable D2H blocks the host)
+        std::vector<std::pair<int, int>> units;
+        if (wavefront) {
+            for (int wave = 0; wave < nbk + nq - 1; ++wave)
+                for (int b = std::max(0, wave - nq + 1); b <= std::min(nbk - 1, wave); ++b) units.push_back({b, wave - b});
+        } else {
+            for (int b = 0; b < nbk; ++b)
+                for (int q = 0; q < nq; ++q) units.push_back({b, q});
+        }
+        {
+            for (auto [b, q] : units) {
+                const i64 j0 = ncut[static_cast<std::size_t>(b)], w = ncut[static_cast<std::size_t>(b) + 1] - j0;
+                const i64 p0 = kcut[static_cast<std::size_t>(q)], kq = kcut[static_cast<std::size_t>(q) + 1] - p0;
+                if (q == 0) {
+                    cuda_check(cudaMemcpyAsync(plan->dC + j0 * e.m, C + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
+                                               cudaMemcpyHostToDevice, cs),
+                               "H2D C block");
+                    cuda_check(cudaEventRecord(evC[b], cs), "event");
+                }
+                if (!have_a[static_cast<std::size_t>(q)]) {
+                    have_a[static_cast<std::size_t>(q)] = 1;
                     cuda_check(cudaMemcpyAsync(plan->dA + p0 * e.m, A + p0 * e.m,
                                                static_cast<std::size_t>(kq * e.m) * 8, cudaMemcpyHostToDevice, cs),
                                "H2D A chunk");
@@ -845,11 +904,15 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
                 tasks += pq->last_tasks;
                 launches += pq->last_launches;
                 ctas = pq->last_ctas;
+                for (int f : finished) d2h(f);
+                finished.clear();
+                if (q == nq - 1) {
+                    cuda_check(cudaEventRecord(evDone[b], st), "event");
+                    finished.push_back(b);
+                }
             }
-            cuda_check(cudaEventRecord(evDone[b], st), "event");
-            if (b > 0) d2h(b - 1);  // one block behind: a pageable D2H blocks the host until it lands
         }
-        d2h(nbk - 1);
+        for (int f : finished) d2h(f);
         cuda_check(cudaStreamSynchronize(ds), "execute_host sync");
         cuda_check(cudaStreamSynchronize(st), "execute_host sync");
         plan->last_tasks = tasks;

@@ -50,8 +50,9 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 }
 
 // ---- ordering between tasks on the same C region (faithful schedule) ----
+// (fix-up tasks use tile/seq for their own counter protocol: never here)
 __device__ __forceinline__ void wait_turn(const Args& a, const Task& t) {
-    if (t.tile < 0 || t.seq <= 0) return;
+    if (t.fixup != 0 || t.tile < 0 || t.seq <= 0) return;
     if (threadIdx.x == 0) {
         int v;
         for (;;) {
@@ -64,7 +65,7 @@ __device__ __forceinline__ void wait_turn(const Args& a, const Task& t) {
 }
 
 __device__ __forceinline__ void signal_done(const Args& a, const Task& t) {
-    if (t.tile < 0) return;
+    if (t.fixup != 0 || t.tile < 0) return;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
