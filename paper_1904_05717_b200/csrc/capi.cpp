@@ -308,7 +308,7 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
                     tk.k = static_cast<int32_t>(std::min(pr[1] * slab, e.k) - pr[0] * slab);
                     const int32_t s0 = slot0[static_cast<std::size_t>(tile)];
                     const int32_t np = static_cast<int32_t>(pieces[static_cast<std::size_t>(tile)].size());
-                    tk.tile = s0 < 0 ? -1 : counter[static_cast<std::size_t>(tile)];
+                    tk.tile = s0 < 0 ? -1 : -2 - counter[static_cast<std::size_t>(tile)];
                     tk.from_c = pr[0] == 0 ? 1 : 0;
                     if (s0 < 0) {
                         tk.seq = 0;
@@ -421,7 +421,7 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
                     const i64 p0 = part * per;
                     tk.p0 = static_cast<int32_t>(p0);
                     tk.k = static_cast<int32_t>(std::min(per, e.k - p0));
-                    tk.tile = ctr;
+                    tk.tile = -2 - ctr;
                     tk.from_c = part == 0 ? 1 : 0;
                     tk.fixup = part == 0 ? 2 : 1;
                     tk.seq = part == 0 ? used - 1 : 0;

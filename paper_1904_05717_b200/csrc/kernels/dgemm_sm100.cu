@@ -50,9 +50,9 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 }
 
 // ---- ordering between tasks on the same C region (faithful schedule) ----
-// (fix-up tasks use tile/seq for their own counter protocol: never here)
+// (fix-up tasks carry tile = -2 - counter, so this protocol skips them)
 __device__ __forceinline__ void wait_turn(const Args& a, const Task& t) {
-    if (t.fixup != 0 || t.tile < 0 || t.seq <= 0) return;
+    if (t.tile < 0 || t.seq <= 0) return;
     if (threadIdx.x == 0) {
         int v;
         for (;;) {
@@ -65,7 +65,7 @@ __device__ __forceinline__ void wait_turn(const Args& a, const Task& t) {
 }
 
 __device__ __forceinline__ void signal_done(const Args& a, const Task& t) {
-    if (t.fixup != 0 || t.tile < 0) return;
+    if (t.tile < 0) return;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -81,7 +81,7 @@ __device__ __forceinline__ void signal_partial(const Args& a, const Task& t) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.progress + t.tile) : "memory");
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.progress + (-2 - t.tile)) : "memory");
     }
 }
 
@@ -89,13 +89,14 @@ template <int FM, int FN>
 __device__ __forceinline__ void fold_partials(const Args& a, const Task& t, double (&acc)[FM][FN][2], int wm0,
                                               int wn0, int g, int tq) {
     if (threadIdx.x == 0) {
+        int32_t* ctr = a.progress + (-2 - t.tile);
         int v;
         for (;;) {
-            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(a.progress + t.tile) : "memory");
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
             if (v >= t.seq) break;
             __nanosleep(64);
         }
-        a.progress[t.tile] = 0;  // every contribution is in: ready for the next launch
+        *ctr = 0;  // every contribution is in: ready for the next launch
     }
     __syncthreads();
     for (int q = 0; q < t.seq; ++q) {

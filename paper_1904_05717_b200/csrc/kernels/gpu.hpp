@@ -23,10 +23,11 @@ struct Task {
     // In-kernel split-k fix-up (DMMA kernels; replaces the reduce launch):
     //   0 — none (slice semantics above);
     //   1 — contributor: the part's partial goes to workspace slot `slice`,
-    //       then counter `tile` is incremented (release);
+    //       then counter (-2 - tile) is incremented (release);
     //   2 — owner (the part that starts from C): after its k loop it waits
-    //       until counter `tile` reaches `seq`, adds slots slice .. slice+seq-1
-    //       in slot order, writes C and resets the counter to 0.
+    //       until counter (-2 - tile) reaches `seq`, adds slots slice ..
+    //       slice+seq-1 in slot order, writes C and resets the counter to 0.
+    //   (tile < 0 keeps fix-up tasks out of the faithful-order protocol.)
     int32_t fixup;
 };
 
