@@ -294,7 +294,7 @@ def our_arm(args):
         dt = (time.perf_counter() - t0) / e2e_steps
         e2e = {"value": flops / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 8 * (m * k + k * n + m * n),
                "d2h_bytes_per_step": 8 * m * n, "ms_per_step": dt * 1e3,
-               "path": "tm_execute_host (pinned host A,B,C -> device, C back)"}
+               "path": "tm_execute_host (pinned host A,B,C -> device, C back; one persistent launch fed by the copy engine)"}
         del Ah, Bh, Ch
 
     # ---- CPU baseline: the reference's execute() on the host cores

@@ -17,6 +17,7 @@
 // value, which is what makes the result independent of the schedule.
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -25,6 +26,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/tilemul_b200.h"
@@ -135,6 +137,23 @@ struct Key {
 
 }  // namespace
 
+// Copy-engine-fed host pipeline (tm_execute_host): one persistent launch
+// over the tasks of every (C column block, k-chunk) unit; the copy stream
+// writes a per-unit flag after the unit's uploads, tasks wait on it, and
+// the download of a block waits on its completion counter.
+struct HostPipe {
+    tm_exec_opts opts{};
+    std::vector<i64> kcut, ncut;
+    std::vector<std::pair<int, int>> units;  // (block, chunk) in issue order
+    std::vector<int32_t> block_tasks;        // tasks of each block's last unit
+    std::unique_ptr<Schedule> sched;
+    int32_t* flags = nullptr;  // [units] data-ready flags, then [blocks] done counters
+    int regions = 0;
+    ~HostPipe() {
+        if (flags) cudaFree(flags);
+    }
+};
+
 struct tm_plan {
     Nest nest;
     Hierarchy hier;
@@ -147,6 +166,7 @@ struct tm_plan {
     // sub-plans of the host-buffer pipeline, keyed by (n, k) extent of one
     // (column block, k-chunk) piece: same family and blocksizes
     std::map<std::pair<int64_t, int64_t>, std::unique_ptr<tm_plan>> chunk_plans;
+    std::unique_ptr<HostPipe> pipe;
     int64_t last_tasks = 0;
     int32_t last_launches = 0, last_ctas = 0;
     ~tm_plan() {
@@ -218,7 +238,8 @@ void alloc_fixup(Schedule& s, const gpu::KernelInfo& info, int32_t slots, int32_
     s.counters = counters;
 }
 
-std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, cudaStream_t stream) {
+std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, cudaStream_t stream,
+                                bool upload = true) {
     auto s = std::make_unique<Schedule>();
     s->kernel = kernel;
     gpu::KernelInfo info{};
@@ -486,6 +507,7 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
         fail_usage("unknown schedule");
     }
     if (T.size() > static_cast<std::size_t>(INT32_MAX)) fail_usage("too many tasks");
+    if (!upload) return s;  // host task list only (callers that splice task lists)
     // Persistent grid: every CTA must be co-resident for the faithful
     // schedule's waits to make progress.
     int grid = o.ctas > 0 ? std::min(o.ctas, slots) : slots;
@@ -541,6 +563,207 @@ void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t l
     plan->last_tasks = static_cast<int64_t>(s.host_tasks.size());
     plan->last_launches = launches;
     plan->last_ctas = s.grid;
+}
+
+// ---------------------------------------------- copy-engine-fed pipeline
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct MemOps {
+    StreamValueFn write = nullptr, wait = nullptr;
+};
+// cuStreamWriteValue32 / cuStreamWaitValue32 through the runtime's driver
+// entry point (the library links the static runtime, not libcuda); null
+// when the driver does not provide them.
+const MemOps& memops() {
+    static const MemOps m = [] {
+        MemOps r;
+        void* fw = nullptr;
+        void* fv = nullptr;
+        cudaDriverEntryPointQueryResult qw{}, qv{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fw, cudaEnableDefault, &qw) == cudaSuccess &&
+            qw == cudaDriverEntryPointSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWaitValue32", &fv, cudaEnableDefault, &qv) == cudaSuccess &&
+            qv == cudaDriverEntryPointSuccess) {
+            r.write = reinterpret_cast<StreamValueFn>(fw);
+            r.wait = reinterpret_cast<StreamValueFn>(fv);
+        }
+        return r;
+    }();
+    return m;
+}
+
+void cu_check(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) throw Failure(kDevice, "", std::string(what) + ": CUresult " + std::to_string(static_cast<int>(r)));
+}
+
+// Cut points of [0, total) into `pieces` equal pieces, aligned.
+std::vector<i64> even_cuts(i64 total, int pieces, i64 align) {
+    const i64 each = cdiv(cdiv(total, std::max(1, pieces)), align) * align;
+    std::vector<i64> start{0};
+    while (start.back() < total) start.push_back(std::min(total, start.back() + each));
+    return start;
+}
+
+// Lowers every unit's sub-nest (fused, unsplit) and splices the task lists
+// into one, in unit order, with global coordinates; each task waits for its
+// unit's data flag and for the previous chunk of its C tile (progress
+// counters, as in the faithful schedule), so every C entry still sees its k
+// chunks in ascending order.
+std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o, cudaStream_t st) {
+    const Extents& e = plan.nest.ext;
+    auto P = std::make_unique<HostPipe>();
+    P->opts = o;
+    // k-chunks of >= 4096 (at most 4) and column blocks of >= 256 (at most
+    // 64): at 16384^3 on PCIe Gen5 these measured best among 4..16 chunks x
+    // 8..64 blocks (tools/e2e_probe.py); smaller k-chunks cost more C round
+    // trips, larger first pieces delay the first GEMM.
+    P->kcut = even_cuts(e.k, static_cast<int>(std::max<i64>(1, std::min<i64>(4, e.k / 4096))), 32);
+    P->ncut = even_cuts(e.n, static_cast<int>(std::max<i64>(1, std::min<i64>(64, e.n / 256))), 128);
+    const int nq = static_cast<int>(P->kcut.size()) - 1, nbk = static_cast<int>(P->ncut.size()) - 1;
+    // Growing-rectangle order: after (A_0, C_0), load next whichever of the
+    // next A k-chunk or the next C column block enables more GEMM work per
+    // byte copied, then run the (block, chunk) units it enables: a new A
+    // chunk adds column q for every loaded block, a new C block adds row b
+    // for every loaded chunk (ascending q, so each C entry still sees its k
+    // chunks in order). Early on this keeps the copy stream ahead of the
+    // math instead of front-loading all of A.
+    {
+        int na = 1, nc = 1;
+        P->units.push_back({0, 0});
+        const double mm = static_cast<double>(e.m);
+        while (na < nq || nc < nbk) {
+            const double kq = static_cast<double>(na < nq ? P->kcut[static_cast<std::size_t>(na) + 1] - P->kcut[static_cast<std::size_t>(na)] : 1);
+            const double wb = static_cast<double>(nc < nbk ? P->ncut[static_cast<std::size_t>(nc) + 1] - P->ncut[static_cast<std::size_t>(nc)] : 1);
+            const double wavg = static_cast<double>(P->ncut[static_cast<std::size_t>(nc)]) / nc;   // loaded columns per block
+            const double kavg = static_cast<double>(P->kcut[static_cast<std::size_t>(na)]) / na;  // loaded k per chunk
+            // flops per byte of the copies each choice needs
+            const double ra = na < nq ? (nc * mm * kq * wavg) / (mm * kq + nc * kq * wavg) : -1.0;
+            const double rc = nc < nbk ? (na * mm * kavg * wb) / (mm * wb + na * kavg * wb) : -1.0;
+            if (ra > rc) {
+                for (int b2 = 0; b2 < nc; ++b2) P->units.push_back({b2, na});
+                ++na;
+            } else {
+                for (int q2 = 0; q2 < na; ++q2) P->units.push_back({nc, q2});
+                ++nc;
+            }
+        }
+    }
+    tm_exec_opts uo = o;
+    uo.split_k = 1;
+    Nest first = plan.nest;
+    first.ext.n = P->ncut[1];
+    first.ext.k = P->kcut[1];
+    const gpu::Kernel kernel = pick_kernel(first, uo);
+    gpu::KernelInfo info{};
+    cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
+    const i64 mt = cdiv(e.m, info.tile_m);
+    P->regions = static_cast<int>(mt * cdiv(e.n, info.tile_n));
+    P->block_tasks.assign(static_cast<std::size_t>(nbk), 0);
+    auto sched = std::make_unique<Schedule>();
+    sched->kernel = kernel;
+    auto& T = sched->host_tasks;
+    for (std::size_t u = 0; u < P->units.size(); ++u) {
+        const auto [b, q] = P->units[u];
+        const i64 j0 = P->ncut[static_cast<std::size_t>(b)], p0 = P->kcut[static_cast<std::size_t>(q)];
+        Nest sn = plan.nest;
+        sn.ext.n = P->ncut[static_cast<std::size_t>(b) + 1] - j0;
+        sn.ext.k = P->kcut[static_cast<std::size_t>(q) + 1] - p0;
+        const auto part = lower(sn, uo, kernel, st, false);
+        for (gpu::Task tk : part->host_tasks) {
+            tk.j0 += static_cast<int32_t>(j0);
+            tk.p0 += static_cast<int32_t>(p0);
+            tk.tile = static_cast<int32_t>(tk.i0 / info.tile_m + (tk.j0 / info.tile_n) * mt);
+            tk.seq = q;
+            tk.ready = static_cast<int32_t>(u) + 1;
+            tk.done = q == nq - 1 ? b + 1 : 0;
+            T.push_back(tk);
+        }
+        if (q == nq - 1) P->block_tasks[static_cast<std::size_t>(b)] = static_cast<int32_t>(part->host_tasks.size());
+    }
+    if (T.size() > static_cast<std::size_t>(INT32_MAX)) fail_usage("too many tasks");
+    sched->grid = std::max(1, std::min<int>(sm_count() * std::max(1, info.ctas_per_sm), static_cast<int>(T.size())));
+    sched->regions = P->regions;
+    cuda_check(cudaGetDevice(&sched->device), "cudaGetDevice");
+    cuda_check(cudaMalloc(&sched->progress, sizeof(int32_t) * static_cast<std::size_t>(P->regions)), "cudaMalloc(progress)");
+    cuda_check(cudaMalloc(&sched->tasks, sizeof(gpu::Task) * T.size()), "cudaMalloc(tasks)");
+    cuda_check(cudaMemcpyAsync(sched->tasks, T.data(), sizeof(gpu::Task) * T.size(), cudaMemcpyHostToDevice, st),
+               "upload tasks");
+    cuda_check(cudaMalloc(&P->flags, sizeof(int32_t) * (P->units.size() + static_cast<std::size_t>(nbk))),
+               "cudaMalloc(pipeline flags)");
+    cuda_check(cudaStreamSynchronize(st), "upload tasks (sync)");
+    P->sched = std::move(sched);
+    return P;
+}
+
+bool same_opts(const tm_exec_opts& a, const tm_exec_opts& b) {
+    return a.numerics == b.numerics && a.schedule == b.schedule && a.split_k == b.split_k && a.ctas == b.ctas &&
+           a.tile == b.tile && a.tile_n == b.tile_n;
+}
+
+void run_pipe(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts& o) {
+    const Extents& e = plan->nest.ext;
+    cudaStream_t st = plan->host_stream, cs = plan->copy_stream, ds = plan->d2h_stream;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (!plan->pipe || !same_opts(plan->pipe->opts, o) || plan->pipe->sched->device != dev)
+        plan->pipe = build_pipe(*plan, o, st);
+    HostPipe& P = *plan->pipe;
+    Schedule& S = *P.sched;
+    const std::size_t nu = P.units.size(), nbk = P.ncut.size() - 1;
+    if (plan->chunk_ready.empty()) {
+        cudaEvent_t ev;
+        cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+        plan->chunk_ready.push_back(ev);
+    }
+    cudaEvent_t zero = plan->chunk_ready[0];
+    cuda_check(cudaMemsetAsync(S.progress, 0, sizeof(int32_t) * static_cast<std::size_t>(P.regions), st), "reset progress");
+    cuda_check(cudaMemsetAsync(P.flags, 0, sizeof(int32_t) * (nu + nbk), st), "reset flags");
+    cuda_check(cudaEventRecord(zero, st), "event");
+    const bool vec16 = e.m % 2 == 0 && e.k % 2 == 0 && origins_even(S.host_tasks);
+    gpu::Args a{plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, S.tasks, static_cast<int32_t>(S.host_tasks.size()),
+                S.progress, nullptr, 0, 0, nullptr, P.flags, P.flags + nu};
+    cuda_check(gpu::launch(S.kernel, vec16, a, S.grid, st), "pipeline kernel launch");
+
+    // uploads in first-need order, a flag after each unit's pieces
+    const std::size_t ldb = static_cast<std::size_t>(e.k) * sizeof(double);
+    cuda_check(cudaStreamWaitEvent(cs, zero, 0), "wait flags reset");
+    std::vector<char> have_a(P.kcut.size(), 0);
+    for (std::size_t u = 0; u < nu; ++u) {
+        const auto [b, q] = P.units[u];
+        const i64 j0 = P.ncut[static_cast<std::size_t>(b)], w = P.ncut[static_cast<std::size_t>(b) + 1] - j0;
+        const i64 p0 = P.kcut[static_cast<std::size_t>(q)], kq = P.kcut[static_cast<std::size_t>(q) + 1] - p0;
+        if (q == 0)
+            cuda_check(cudaMemcpyAsync(plan->dC + j0 * e.m, C + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
+                                       cudaMemcpyHostToDevice, cs),
+                       "H2D C block");
+        if (!have_a[static_cast<std::size_t>(q)]) {
+            have_a[static_cast<std::size_t>(q)] = 1;
+            cuda_check(cudaMemcpyAsync(plan->dA + p0 * e.m, A + p0 * e.m, static_cast<std::size_t>(kq * e.m) * 8,
+                                       cudaMemcpyHostToDevice, cs),
+                       "H2D A chunk");
+        }
+        cuda_check(cudaMemcpy2DAsync(plan->dB + p0 + j0 * e.k, ldb, B + p0 + j0 * e.k, ldb,
+                                     static_cast<std::size_t>(kq) * 8, static_cast<std::size_t>(w),
+                                     cudaMemcpyHostToDevice, cs),
+                   "H2D B piece");
+        cu_check(memops().write(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(P.flags + u), 1, 0),
+                 "cuStreamWriteValue32");
+    }
+    // each block goes back once its last unit's tasks are done
+    cuda_check(cudaStreamWaitEvent(ds, zero, 0), "wait flags reset");
+    for (std::size_t b = 0; b < nbk; ++b) {
+        const i64 j0 = P.ncut[b], w = P.ncut[b + 1] - j0;
+        cu_check(memops().wait(reinterpret_cast<CUstream>(ds), reinterpret_cast<CUdeviceptr>(P.flags + nu + b),
+                               static_cast<cuuint32_t>(P.block_tasks[b]), CU_STREAM_WAIT_VALUE_GEQ),
+                 "cuStreamWaitValue32");
+        cuda_check(cudaMemcpyAsync(C + j0 * e.m, plan->dC + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
+                                   cudaMemcpyDeviceToHost, ds),
+                   "D2H C block");
+    }
+    cuda_check(cudaStreamSynchronize(ds), "execute_host sync");
+    cuda_check(cudaStreamSynchronize(st), "execute_host sync");
+    plan->last_tasks = static_cast<int64_t>(S.host_tasks.size());
+    plan->last_launches = 1;
+    plan->last_ctas = S.grid;
 }
 
 }  // namespace
@@ -770,63 +993,22 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
             cuda_check(cudaStreamSynchronize(st), "execute_host sync");
             return;
         }
-        // Copy/compute pipeline over (C column block b, k-chunk q) units in
-        // wavefront order (b + q ascending): uploads are issued on one copy
-        // stream in the order the GEMMs first need them (C_b, A_q, B_qb), so
-        // the data the first GEMMs wait for grows with the work they do
-        // instead of all of A arriving during column block 0; a finished
-        // block goes back on a third stream while the rest computes. Every C
-        // entry still sees its k chunks in ascending order (chunks are
+        // Copy/compute pipeline over (C column block, k-chunk) units; every
+        // C entry still sees its k chunks in ascending order (chunks are
         // multiples of the 32-deep slab), i.e. exactly the unpipelined
-        // operation sequence.
+        // operation sequence. Preferred: one persistent launch fed by the
+        // copy engine (run_pipe).
         mkstream(plan->copy_stream);
         mkstream(plan->d2h_stream);
-        int nq0 = e.k >= 4096 ? static_cast<int>(std::min<i64>(8, e.k / 2048)) : 1;
-        int nb0 = e.n >= 2048 ? static_cast<int>(std::min<i64>(8, e.n / 1024)) : 1;
-        if (const char* v = std::getenv("TM_PIPE_NQ")) nq0 = std::max(1, std::atoi(v));
-        if (const char* v = std::getenv("TM_PIPE_NB")) nb0 = std::max(1, std::atoi(v));
-        const bool taper = std::getenv("TM_PIPE_TAPER") ? std::atoi(std::getenv("TM_PIPE_TAPER")) != 0 : true;
-        const bool wavefront = std::getenv("TM_PIPE_WAVE") ? std::atoi(std::getenv("TM_PIPE_WAVE")) != 0 : true;
-        const i64 kc = cdiv(cdiv(e.k, nq0), 32) * 32;
-        const i64 wb = cdiv(cdiv(e.n, nb0), 128) * 128;
-        // Tapered pieces: the first k-chunks and the first and last column
-        // blocks are 1/4 and 1/2 of the regular size, so the copies the first
-        // GEMM waits for, and the last block's download, are small.
-        auto cuts = [](i64 total, i64 base, i64 align, bool taper_end) {
-            std::vector<i64> sz;
-            const i64 q4 = std::max(align, base / 4 / align * align), q2 = std::max(align, base / 2 / align * align);
-            std::vector<i64> head{q4, q2}, tail;
-            if (taper_end) tail = {q2, q4};
-            i64 left = total;
-            for (i64 h : head)
-                if (left > h + base) {
-                    sz.push_back(h);
-                    left -= h;
-                }
-            std::vector<i64> end;
-            for (i64 t : tail)
-                if (left > t + base) {
-                    end.insert(end.begin(), t);
-                    left -= t;
-                }
-            const i64 nmid = cdiv(left, base), each = cdiv(cdiv(left, nmid), align) * align;
-            while (left > 0) {  // the middle in equal aligned pieces (no sliver)
-                const i64 x = std::min(each, left);
-                sz.push_back(x);
-                left -= x;
-            }
-            sz.insert(sz.end(), end.begin(), end.end());
-            std::vector<i64> start{0};
-            for (i64 x : sz) start.push_back(start.back() + x);
-            return start;  // piece i = [start[i], start[i+1])
-        };
-        auto plain = [](i64 total, i64 base) {
-            std::vector<i64> st{0};
-            while (st.back() < total) st.push_back(std::min(total, st.back() + base));
-            return st;
-        };
-        const std::vector<i64> kcut = nq0 > 1 ? (taper ? cuts(e.k, kc, 32, false) : plain(e.k, kc)) : std::vector<i64>{0, e.k};
-        const std::vector<i64> ncut = nb0 > 1 ? (taper ? cuts(e.n, wb, 128, true) : plain(e.n, wb)) : std::vector<i64>{0, e.n};
+        if (memops().write && memops().wait) {
+            run_pipe(plan, A, B, C, o);
+            return;
+        }
+        // Fallback (driver without stream memory operations): one launch per
+        // unit, units in wavefront order (b + q ascending), uploads on one
+        // copy stream in first-need order, downloads on a third stream.
+        const std::vector<i64> kcut = even_cuts(e.k, e.k >= 4096 ? static_cast<int>(std::min<i64>(8, e.k / 2048)) : 1, 32);
+        const std::vector<i64> ncut = even_cuts(e.n, e.n >= 2048 ? static_cast<int>(std::min<i64>(16, e.n / 1024)) : 1, 128);
         const int nq = static_cast<int>(kcut.size()) - 1;
         const int nbk = static_cast<int>(ncut.size()) - 1;
         const std::size_t nev = static_cast<std::size_t>(nq + 2 * nbk + nbk * nq);
@@ -864,13 +1046,8 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
         std::vector<char> have_a(static_cast<std::size_t>(nq), 0);
         std::vector<int> finished;  // blocks whose D2H is issued one unit later (a pageable D2H blocks the host)
         std::vector<std::pair<int, int>> units;
-        if (wavefront) {
-            for (int wave = 0; wave < nbk + nq - 1; ++wave)
-                for (int b = std::max(0, wave - nq + 1); b <= std::min(nbk - 1, wave); ++b) units.push_back({b, wave - b});
-        } else {
-            for (int b = 0; b < nbk; ++b)
-                for (int q = 0; q < nq; ++q) units.push_back({b, q});
-        }
+        for (int wave = 0; wave < nbk + nq - 1; ++wave)
+            for (int b = std::max(0, wave - nq + 1); b <= std::min(nbk - 1, wave); ++b) units.push_back({b, wave - b});
         {
             for (auto [b, q] : units) {
                 const i64 j0 = ncut[static_cast<std::size_t>(b)], w = ncut[static_cast<std::size_t>(b) + 1] - j0;

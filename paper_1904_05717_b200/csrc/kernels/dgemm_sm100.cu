@@ -64,13 +64,33 @@ __device__ __forceinline__ void wait_turn(const Args& a, const Task& t) {
     __syncthreads();
 }
 
-__device__ __forceinline__ void signal_done(const Args& a, const Task& t) {
+__device__ __forceinline__ void signal_done(const Args& a, const Task& t, int ti) {
     if (t.tile < 0) return;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(a.progress + t.tile), "r"(t.seq + 1) : "memory");
+        if (a.done) {  // pipeline: count the block's finished tiles (the D2H copy waits on it)
+            const int dn = a.tasks[ti].done;
+            if (dn > 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.done + dn - 1) : "memory");
+        }
     }
+}
+
+// Copy-engine-fed pipeline: the task's inputs are in HBM once the copy stream
+// has written its flag (cuStreamWriteValue32 after the copies, in order).
+__device__ __forceinline__ void wait_ready(const Args& a, const Task& t) {
+    if (t.ready == 0) return;
+    if (threadIdx.x == 0) {
+        const int32_t* f = a.ready + t.ready - 1;
+        int v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+            if (v != 0) break;
+            __nanosleep(256);
+        }
+    }
+    __syncthreads();
 }
 
 // Split-k fix-up inside the task kernel (Task::fixup). Contributors publish
@@ -322,6 +342,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
     const int t_step = a.cta_first ? 1 : static_cast<int>(gridDim.x);
     for (int ti = t_lo; ti < t_hi; ti += t_step) {
         const Task t = a.tasks[ti];
+        wait_ready(a, t);
         wait_turn(a, t);
         const int nk = (t.k + BK - 1) / BK;
         S st;
@@ -422,7 +443,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
                 }
             }
         if (FIX && t.fixup == 1) signal_partial(a, t);
-        else signal_done(a, t);
+        else signal_done(a, t, ti);
     }
 }
 
@@ -443,6 +464,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN)) k_simt(Args a) {
     const int t_step = a.cta_first ? 1 : static_cast<int>(gridDim.x);
     for (int ti = t_lo; ti < t_hi; ti += t_step) {
         const Task t = a.tasks[ti];
+        wait_ready(a, t);
         wait_turn(a, t);
         const int nk = (t.k + kBK - 1) / kBK;
 #pragma unroll
@@ -509,7 +531,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN)) k_simt(Args a) {
                 if (r < t.m && c < t.n)
                     d.dst[(d.oi + r) + (d.oj + c) * d.ld_dst] = acc[i][j];
             }
-        signal_done(a, t);
+        signal_done(a, t, ti);
     }
 }
 

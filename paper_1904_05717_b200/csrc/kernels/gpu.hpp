@@ -29,6 +29,12 @@ struct Task {
     //       slice+seq-1 in slot order, writes C and resets the counter to 0.
     //   (tile < 0 keeps fix-up tasks out of the faithful-order protocol.)
     int32_t fixup;
+    // Copy-engine-fed pipeline (tm_execute_host): ready = 1 + index of the
+    // data flag the task waits for before touching A/B/C (0 = none); done =
+    // 1 + index of the counter it increments once its C tile is final
+    // (0 = none). Both are read only at task boundaries.
+    int32_t ready;
+    int32_t done;
 };
 
 struct Args {
@@ -46,6 +52,8 @@ struct Args {
     int64_t work_slice;  // elements per slot
     const int32_t* cta_first;  // blocked assignment: CTA c runs tasks [cta_first[c], cta_first[c+1]);
                                // nullptr = strided (task t on CTA t mod grid)
+    const int32_t* ready;      // data flags written by the copy stream (Task::ready), or nullptr
+    int32_t* done;             // per-block completion counters (Task::done), or nullptr
 };
 
 // One k-split C tile: its partials live in slots slot0 .. slot0+nslots-1 and
