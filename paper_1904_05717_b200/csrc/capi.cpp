@@ -159,6 +159,7 @@ struct tm_plan {
     Hierarchy hier;
     std::map<Key, std::unique_ptr<Schedule>> schedules;
     std::mutex mu;
+    std::mutex host_mu;  // one tm_execute_host at a time per plan (it owns the plan's staging buffers and streams)
     // host-buffer execution
     double *dA = nullptr, *dB = nullptr, *dC = nullptr;
     cudaStream_t host_stream = nullptr, copy_stream = nullptr, d2h_stream = nullptr;
@@ -968,6 +969,7 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
     return guard([&] {
         if (!plan) fail_usage("null plan");
         if (!A || !B || !C) fail_usage("null operand pointer");
+        std::lock_guard<std::mutex> hold(plan->host_mu);
         const Extents& e = plan->nest.ext;
         const std::size_t na = static_cast<std::size_t>(e.m * e.k), nb = static_cast<std::size_t>(e.k * e.n),
                           nc = static_cast<std::size_t>(e.m * e.n);
