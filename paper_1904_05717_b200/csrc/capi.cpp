@@ -592,6 +592,16 @@ const MemOps& memops() {
     return m;
 }
 
+// The persistent pipeline's tasks wait on flags written by another stream's
+// copies: that needs the kernel and the copies to run concurrently, which
+// CUDA_LAUNCH_BLOCKING=1 (the launch returns only when the kernel is done)
+// and injected tools that serialize GPU work (Nsight Compute, sanitizers:
+// CUDA_INJECTION64_PATH) rule out. Those get the one-launch-per-unit path.
+bool serialized_launches() {
+    const char* lb = std::getenv("CUDA_LAUNCH_BLOCKING");
+    return (lb != nullptr && std::atoi(lb) != 0) || std::getenv("CUDA_INJECTION64_PATH") != nullptr;
+}
+
 void cu_check(CUresult r, const char* what) {
     if (r != CUDA_SUCCESS) throw Failure(kDevice, "", std::string(what) + ": CUresult " + std::to_string(static_cast<int>(r)));
 }
@@ -1002,7 +1012,7 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
         // copy engine (run_pipe).
         mkstream(plan->copy_stream);
         mkstream(plan->d2h_stream);
-        if (memops().write && memops().wait) {
+        if (memops().write && memops().wait && !serialized_launches()) {
             run_pipe(plan, A, B, C, o);
             return;
         }
