@@ -1,0 +1,125 @@
+// Internal interface between the C ABI (capi.cpp), the lowering of a loop
+// nest onto CTA tasks (lower.cpp) and the host-buffer pipelines
+// (host_pipe.cpp). Not installed; callers use include/tilemul_b200.h.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/tilemul_b200.h"
+#include "host/mmm.hpp"
+#include "kernels/gpu.hpp"
+
+namespace mmm {
+namespace engine {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Failure(kDevice, "", std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct Schedule {
+    gpu::Kernel kernel = gpu::kDmma128;
+    bool vec16 = false;
+    int grid = 1;
+    int slices = 0;          // number of k-split tiles to reduce (fused)
+    gpu::ReduceTile* reduce = nullptr;
+    int32_t* cta_first = nullptr;  // stream-K: per-CTA task ranges
+    bool blocked = false;
+    int grid_fixed = 0;
+    int regions = 0;         // progress counters (faithful)
+    int counters = 0;        // split-k fix-up counters (DMMA kernels), self-resetting
+    std::vector<gpu::Task> host_tasks;
+    gpu::Task* tasks = nullptr;
+    int32_t* progress = nullptr;
+    double* work = nullptr;
+    int64_t work_ld = 0, work_slice = 0;
+    int device = -1;
+    ~Schedule() {
+        if (tasks) cudaFree(tasks);
+        if (progress) cudaFree(progress);
+        if (work) cudaFree(work);
+        if (reduce) cudaFree(reduce);
+        if (cta_first) cudaFree(cta_first);
+    }
+};
+
+struct Key {
+    int schedule, kernel, split, ctas;
+    bool vec16;
+    bool operator<(const Key& o) const {
+        return std::tie(schedule, kernel, split, ctas, vec16) < std::tie(o.schedule, o.kernel, o.split, o.ctas, o.vec16);
+    }
+};
+
+// Copy-engine-fed host pipeline (tm_execute_host): one persistent launch
+// over the tasks of every (C column block, k-chunk) unit; the copy stream
+// writes a per-unit flag after the unit's uploads, tasks wait on it, and
+// the download of a block waits on its completion counter.
+struct HostPipe {
+    tm_exec_opts opts{};
+    std::vector<i64> kcut, ncut;
+    std::vector<std::pair<int, int>> units;  // (block, chunk) in issue order
+    std::vector<int32_t> block_tasks;        // tasks of each block's last unit
+    std::unique_ptr<Schedule> sched;
+    int32_t* flags = nullptr;  // [units] data-ready flags, then [blocks] done counters
+    int regions = 0;
+    ~HostPipe() {
+        if (flags) cudaFree(flags);
+    }
+};
+
+int sm_count();
+gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o);
+// Lowers the nest onto CTA tasks for `kernel` (schedule, split and fix-up
+// per opts). upload = false builds the host task list only.
+std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, cudaStream_t stream,
+                                bool upload = true);
+bool origins_even(const std::vector<gpu::Task>& T);
+
+}  // namespace engine
+}  // namespace mmm
+
+// The opaque plan handle of the C ABI.
+struct tm_plan {
+    mmm::Nest nest;
+    mmm::Hierarchy hier;
+    std::map<mmm::engine::Key, std::unique_ptr<mmm::engine::Schedule>> schedules;
+    std::mutex mu;
+    std::mutex host_mu;  // one tm_execute_host at a time per plan (it owns the plan's staging buffers and streams)
+    // host-buffer execution
+    double *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    cudaStream_t host_stream = nullptr, copy_stream = nullptr, d2h_stream = nullptr;
+    std::vector<cudaEvent_t> chunk_ready;
+    // sub-plans of the host-buffer pipeline, keyed by (n, k) extent of one
+    // (column block, k-chunk) piece: same family and blocksizes
+    std::map<std::pair<int64_t, int64_t>, std::unique_ptr<tm_plan>> chunk_plans;
+    std::unique_ptr<mmm::engine::HostPipe> pipe;
+    int64_t last_tasks = 0;
+    int32_t last_launches = 0, last_ctas = 0;
+    ~tm_plan() {
+        if (dA) cudaFree(dA);
+        if (dB) cudaFree(dB);
+        if (dC) cudaFree(dC);
+        for (auto ev : chunk_ready) cudaEventDestroy(ev);
+        if (host_stream) cudaStreamDestroy(host_stream);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (d2h_stream) cudaStreamDestroy(d2h_stream);
+    }
+};
+
+namespace mmm {
+namespace engine {
+// execute(): device operands, asynchronous on `stream` (tm_execute).
+void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+         const tm_exec_opts* opts, cudaStream_t stream);
+// execute() on host buffers: copies in, runs, copies C back (tm_execute_host).
+void execute_host(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts* opts);
+}  // namespace engine
+}  // namespace mmm

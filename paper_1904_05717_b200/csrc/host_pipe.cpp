@@ -1,0 +1,364 @@
+// Host-buffer execution (tm_execute_host): copies in, the GEMM, C back,
+// pipelined. Preferred: one persistent launch over every (C column block,
+// k-chunk) unit, fed by the copy engine through stream memory operations;
+// fallback: one launch per unit.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include <cuda.h>
+
+#include "engine.hpp"
+
+namespace mmm {
+namespace engine {
+
+namespace {
+
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct MemOps {
+    StreamValueFn write = nullptr, wait = nullptr;
+};
+// cuStreamWriteValue32 / cuStreamWaitValue32 through the runtime's driver
+// entry point (the library links the static runtime, not libcuda); null
+// when the driver does not provide them.
+const MemOps& memops() {
+    static const MemOps m = [] {
+        MemOps r;
+        void* fw = nullptr;
+        void* fv = nullptr;
+        cudaDriverEntryPointQueryResult qw{}, qv{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fw, cudaEnableDefault, &qw) == cudaSuccess &&
+            qw == cudaDriverEntryPointSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWaitValue32", &fv, cudaEnableDefault, &qv) == cudaSuccess &&
+            qv == cudaDriverEntryPointSuccess) {
+            r.write = reinterpret_cast<StreamValueFn>(fw);
+            r.wait = reinterpret_cast<StreamValueFn>(fv);
+        }
+        return r;
+    }();
+    return m;
+}
+
+// The persistent pipeline's tasks wait on flags written by another stream's
+// copies: that needs the kernel and the copies to run concurrently, which
+// CUDA_LAUNCH_BLOCKING=1 (the launch returns only when the kernel is done)
+// and injected tools that serialize GPU work (Nsight Compute, sanitizers:
+// CUDA_INJECTION64_PATH) rule out. Those get the one-launch-per-unit path.
+bool serialized_launches() {
+    const char* lb = std::getenv("CUDA_LAUNCH_BLOCKING");
+    return (lb != nullptr && std::atoi(lb) != 0) || std::getenv("CUDA_INJECTION64_PATH") != nullptr;
+}
+
+void cu_check(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) throw Failure(kDevice, "", std::string(what) + ": CUresult " + std::to_string(static_cast<int>(r)));
+}
+
+// Cut points of [0, total) into `pieces` equal pieces, aligned.
+std::vector<i64> even_cuts(i64 total, int pieces, i64 align) {
+    const i64 each = cdiv(cdiv(total, std::max(1, pieces)), align) * align;
+    std::vector<i64> start{0};
+    while (start.back() < total) start.push_back(std::min(total, start.back() + each));
+    return start;
+}
+
+// Lowers every unit's sub-nest (fused, unsplit) and splices the task lists
+// into one, in unit order, with global coordinates; each task waits for its
+// unit's data flag and for the previous chunk of its C tile (progress
+// counters, as in the faithful schedule), so every C entry still sees its k
+// chunks in ascending order.
+std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o, cudaStream_t st) {
+    const Extents& e = plan.nest.ext;
+    auto P = std::make_unique<HostPipe>();
+    P->opts = o;
+    // k-chunks of >= 4096 (at most 4) and column blocks of >= 256 (at most
+    // 64): at 16384^3 on PCIe Gen5 these measured best among 4..16 chunks x
+    // 8..64 blocks (tools/e2e_probe.py); smaller k-chunks cost more C round
+    // trips, larger first pieces delay the first GEMM.
+    P->kcut = even_cuts(e.k, static_cast<int>(std::max<i64>(1, std::min<i64>(4, e.k / 4096))), 32);
+    P->ncut = even_cuts(e.n, static_cast<int>(std::max<i64>(1, std::min<i64>(64, e.n / 256))), 128);
+    const int nq = static_cast<int>(P->kcut.size()) - 1, nbk = static_cast<int>(P->ncut.size()) - 1;
+    // Growing-rectangle order: after (A_0, C_0), load next whichever of the
+    // next A k-chunk or the next C column block enables more GEMM work per
+    // byte copied, then run the (block, chunk) units it enables: a new A
+    // chunk adds column q for every loaded block, a new C block adds row b
+    // for every loaded chunk (ascending q, so each C entry still sees its k
+    // chunks in order). Early on this keeps the copy stream ahead of the
+    // math instead of front-loading all of A.
+    {
+        int na = 1, nc = 1;
+        P->units.push_back({0, 0});
+        const double mm = static_cast<double>(e.m);
+        while (na < nq || nc < nbk) {
+            const double kq = static_cast<double>(na < nq ? P->kcut[static_cast<std::size_t>(na) + 1] - P->kcut[static_cast<std::size_t>(na)] : 1);
+            const double wb = static_cast<double>(nc < nbk ? P->ncut[static_cast<std::size_t>(nc) + 1] - P->ncut[static_cast<std::size_t>(nc)] : 1);
+            const double wavg = static_cast<double>(P->ncut[static_cast<std::size_t>(nc)]) / nc;   // loaded columns per block
+            const double kavg = static_cast<double>(P->kcut[static_cast<std::size_t>(na)]) / na;  // loaded k per chunk
+            // flops per byte of the copies each choice needs
+            const double ra = na < nq ? (nc * mm * kq * wavg) / (mm * kq + nc * kq * wavg) : -1.0;
+            const double rc = nc < nbk ? (na * mm * kavg * wb) / (mm * wb + na * kavg * wb) : -1.0;
+            if (ra > rc) {
+                for (int b2 = 0; b2 < nc; ++b2) P->units.push_back({b2, na});
+                ++na;
+            } else {
+                for (int q2 = 0; q2 < na; ++q2) P->units.push_back({nc, q2});
+                ++nc;
+            }
+        }
+    }
+    tm_exec_opts uo = o;
+    uo.split_k = 1;
+    Nest first = plan.nest;
+    first.ext.n = P->ncut[1];
+    first.ext.k = P->kcut[1];
+    const gpu::Kernel kernel = pick_kernel(first, uo);
+    gpu::KernelInfo info{};
+    cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
+    const i64 mt = cdiv(e.m, info.tile_m);
+    P->regions = static_cast<int>(mt * cdiv(e.n, info.tile_n));
+    P->block_tasks.assign(static_cast<std::size_t>(nbk), 0);
+    auto sched = std::make_unique<Schedule>();
+    sched->kernel = kernel;
+    auto& T = sched->host_tasks;
+    for (std::size_t u = 0; u < P->units.size(); ++u) {
+        const auto [b, q] = P->units[u];
+        const i64 j0 = P->ncut[static_cast<std::size_t>(b)], p0 = P->kcut[static_cast<std::size_t>(q)];
+        Nest sn = plan.nest;
+        sn.ext.n = P->ncut[static_cast<std::size_t>(b) + 1] - j0;
+        sn.ext.k = P->kcut[static_cast<std::size_t>(q) + 1] - p0;
+        const auto part = lower(sn, uo, kernel, st, false);
+        for (gpu::Task tk : part->host_tasks) {
+            tk.j0 += static_cast<int32_t>(j0);
+            tk.p0 += static_cast<int32_t>(p0);
+            tk.tile = static_cast<int32_t>(tk.i0 / info.tile_m + (tk.j0 / info.tile_n) * mt);
+            tk.seq = q;
+            tk.ready = static_cast<int32_t>(u) + 1;
+            tk.done = q == nq - 1 ? b + 1 : 0;
+            T.push_back(tk);
+        }
+        if (q == nq - 1) P->block_tasks[static_cast<std::size_t>(b)] = static_cast<int32_t>(part->host_tasks.size());
+    }
+    if (T.size() > static_cast<std::size_t>(INT32_MAX)) fail_usage("too many tasks");
+    sched->grid = std::max(1, std::min<int>(sm_count() * std::max(1, info.ctas_per_sm), static_cast<int>(T.size())));
+    sched->regions = P->regions;
+    cuda_check(cudaGetDevice(&sched->device), "cudaGetDevice");
+    cuda_check(cudaMalloc(&sched->progress, sizeof(int32_t) * static_cast<std::size_t>(P->regions)), "cudaMalloc(progress)");
+    cuda_check(cudaMalloc(&sched->tasks, sizeof(gpu::Task) * T.size()), "cudaMalloc(tasks)");
+    cuda_check(cudaMemcpyAsync(sched->tasks, T.data(), sizeof(gpu::Task) * T.size(), cudaMemcpyHostToDevice, st),
+               "upload tasks");
+    cuda_check(cudaMalloc(&P->flags, sizeof(int32_t) * (P->units.size() + static_cast<std::size_t>(nbk))),
+               "cudaMalloc(pipeline flags)");
+    cuda_check(cudaStreamSynchronize(st), "upload tasks (sync)");
+    P->sched = std::move(sched);
+    return P;
+}
+
+bool same_opts(const tm_exec_opts& a, const tm_exec_opts& b) {
+    return a.numerics == b.numerics && a.schedule == b.schedule && a.split_k == b.split_k && a.ctas == b.ctas &&
+           a.tile == b.tile && a.tile_n == b.tile_n;
+}
+
+void run_pipe(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts& o) {
+    const Extents& e = plan->nest.ext;
+    cudaStream_t st = plan->host_stream, cs = plan->copy_stream, ds = plan->d2h_stream;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (!plan->pipe || !same_opts(plan->pipe->opts, o) || plan->pipe->sched->device != dev)
+        plan->pipe = build_pipe(*plan, o, st);
+    HostPipe& P = *plan->pipe;
+    Schedule& S = *P.sched;
+    const std::size_t nu = P.units.size(), nbk = P.ncut.size() - 1;
+    if (plan->chunk_ready.empty()) {
+        cudaEvent_t ev;
+        cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+        plan->chunk_ready.push_back(ev);
+    }
+    cudaEvent_t zero = plan->chunk_ready[0];
+    cuda_check(cudaMemsetAsync(S.progress, 0, sizeof(int32_t) * static_cast<std::size_t>(P.regions), st), "reset progress");
+    cuda_check(cudaMemsetAsync(P.flags, 0, sizeof(int32_t) * (nu + nbk), st), "reset flags");
+    cuda_check(cudaEventRecord(zero, st), "event");
+    const bool vec16 = e.m % 2 == 0 && e.k % 2 == 0 && origins_even(S.host_tasks);
+    gpu::Args a{plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, S.tasks, static_cast<int32_t>(S.host_tasks.size()),
+                S.progress, nullptr, 0, 0, nullptr, P.flags, P.flags + nu};
+    cuda_check(gpu::launch(S.kernel, vec16, a, S.grid, st), "pipeline kernel launch");
+
+    // uploads in first-need order, a flag after each unit's pieces
+    const std::size_t ldb = static_cast<std::size_t>(e.k) * sizeof(double);
+    cuda_check(cudaStreamWaitEvent(cs, zero, 0), "wait flags reset");
+    std::vector<char> have_a(P.kcut.size(), 0);
+    for (std::size_t u = 0; u < nu; ++u) {
+        const auto [b, q] = P.units[u];
+        const i64 j0 = P.ncut[static_cast<std::size_t>(b)], w = P.ncut[static_cast<std::size_t>(b) + 1] - j0;
+        const i64 p0 = P.kcut[static_cast<std::size_t>(q)], kq = P.kcut[static_cast<std::size_t>(q) + 1] - p0;
+        if (q == 0)
+            cuda_check(cudaMemcpyAsync(plan->dC + j0 * e.m, C + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
+                                       cudaMemcpyHostToDevice, cs),
+                       "H2D C block");
+        if (!have_a[static_cast<std::size_t>(q)]) {
+            have_a[static_cast<std::size_t>(q)] = 1;
+            cuda_check(cudaMemcpyAsync(plan->dA + p0 * e.m, A + p0 * e.m, static_cast<std::size_t>(kq * e.m) * 8,
+                                       cudaMemcpyHostToDevice, cs),
+                       "H2D A chunk");
+        }
+        cuda_check(cudaMemcpy2DAsync(plan->dB + p0 + j0 * e.k, ldb, B + p0 + j0 * e.k, ldb,
+                                     static_cast<std::size_t>(kq) * 8, static_cast<std::size_t>(w),
+                                     cudaMemcpyHostToDevice, cs),
+                   "H2D B piece");
+        cu_check(memops().write(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(P.flags + u), 1, 0),
+                 "cuStreamWriteValue32");
+    }
+    // each block goes back once its last unit's tasks are done
+    cuda_check(cudaStreamWaitEvent(ds, zero, 0), "wait flags reset");
+    for (std::size_t b = 0; b < nbk; ++b) {
+        const i64 j0 = P.ncut[b], w = P.ncut[b + 1] - j0;
+        cu_check(memops().wait(reinterpret_cast<CUstream>(ds), reinterpret_cast<CUdeviceptr>(P.flags + nu + b),
+                               static_cast<cuuint32_t>(P.block_tasks[b]), CU_STREAM_WAIT_VALUE_GEQ),
+                 "cuStreamWaitValue32");
+        cuda_check(cudaMemcpyAsync(C + j0 * e.m, plan->dC + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
+                                   cudaMemcpyDeviceToHost, ds),
+                   "D2H C block");
+    }
+    cuda_check(cudaStreamSynchronize(ds), "execute_host sync");
+    cuda_check(cudaStreamSynchronize(st), "execute_host sync");
+    plan->last_tasks = static_cast<int64_t>(S.host_tasks.size());
+    plan->last_launches = 1;
+    plan->last_ctas = S.grid;
+}
+
+}  // namespace
+
+void execute_host(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts* opts) {
+    if (!plan) fail_usage("null plan");
+    if (!A || !B || !C) fail_usage("null operand pointer");
+    std::lock_guard<std::mutex> hold(plan->host_mu);
+    const Extents& e = plan->nest.ext;
+    const std::size_t na = static_cast<std::size_t>(e.m * e.k), nb = static_cast<std::size_t>(e.k * e.n),
+                      nc = static_cast<std::size_t>(e.m * e.n);
+    auto mkstream = [](cudaStream_t& s) {
+        if (!s) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    };
+    mkstream(plan->host_stream);
+    if (!plan->dA) {
+        cuda_check(cudaMalloc(&plan->dA, na * sizeof(double)), "cudaMalloc(A)");
+        cuda_check(cudaMalloc(&plan->dB, nb * sizeof(double)), "cudaMalloc(B)");
+        cuda_check(cudaMalloc(&plan->dC, nc * sizeof(double)), "cudaMalloc(C)");
+    }
+    cudaStream_t st = plan->host_stream;
+    tm_exec_opts o{};
+    if (opts) o = *opts;
+    const bool pipelined = o.schedule == TM_SCHEDULE_FUSED && o.split_k <= 1 && (e.k >= 4096 || e.n >= 4096);
+    if (!pipelined) {
+        cuda_check(cudaMemcpyAsync(plan->dA, A, na * sizeof(double), cudaMemcpyHostToDevice, st), "H2D A");
+        cuda_check(cudaMemcpyAsync(plan->dB, B, nb * sizeof(double), cudaMemcpyHostToDevice, st), "H2D B");
+        cuda_check(cudaMemcpyAsync(plan->dC, C, nc * sizeof(double), cudaMemcpyHostToDevice, st), "H2D C");
+        run(plan, plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, opts, st);
+        cuda_check(cudaMemcpyAsync(C, plan->dC, nc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H C");
+        cuda_check(cudaStreamSynchronize(st), "execute_host sync");
+        return;
+    }
+    // Copy/compute pipeline over (C column block, k-chunk) units; every
+    // C entry still sees its k chunks in ascending order (chunks are
+    // multiples of the 32-deep slab), i.e. exactly the unpipelined
+    // operation sequence. Preferred: one persistent launch fed by the
+    // copy engine (run_pipe).
+    mkstream(plan->copy_stream);
+    mkstream(plan->d2h_stream);
+    if (memops().write && memops().wait && !serialized_launches()) {
+        run_pipe(plan, A, B, C, o);
+        return;
+    }
+    // Fallback (driver without stream memory operations): one launch per
+    // unit, units in wavefront order (b + q ascending), uploads on one
+    // copy stream in first-need order, downloads on a third stream.
+    const std::vector<i64> kcut = even_cuts(e.k, e.k >= 4096 ? static_cast<int>(std::min<i64>(8, e.k / 2048)) : 1, 32);
+    const std::vector<i64> ncut = even_cuts(e.n, e.n >= 2048 ? static_cast<int>(std::min<i64>(16, e.n / 1024)) : 1, 128);
+    const int nq = static_cast<int>(kcut.size()) - 1;
+    const int nbk = static_cast<int>(ncut.size()) - 1;
+    const std::size_t nev = static_cast<std::size_t>(nq + 2 * nbk + nbk * nq);
+    while (plan->chunk_ready.size() < nev) {
+        cudaEvent_t ev;
+        cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+        plan->chunk_ready.push_back(ev);
+    }
+    cudaEvent_t* evA = plan->chunk_ready.data();
+    cudaEvent_t* evC = evA + nq;
+    cudaEvent_t* evDone = evC + nbk;
+    cudaEvent_t* evB = evDone + nbk;
+    auto sub = [&](i64 nn, i64 kk) -> tm_plan* {
+        auto& slot = plan->chunk_plans[{nn, kk}];
+        if (!slot) {
+            slot = std::make_unique<tm_plan>();
+            slot->nest = plan->nest;
+            slot->nest.ext.n = nn;
+            slot->nest.ext.k = kk;
+            slot->hier = plan->hier;
+        }
+        return slot.get();
+    };
+    cudaStream_t cs = plan->copy_stream, ds = plan->d2h_stream;
+    const std::size_t ld = static_cast<std::size_t>(e.k) * sizeof(double);
+    int64_t tasks = 0;
+    int32_t launches = 0, ctas = 0;
+    auto d2h = [&](int b) {
+        const i64 j0 = ncut[static_cast<std::size_t>(b)], w = ncut[static_cast<std::size_t>(b) + 1] - j0;
+        cuda_check(cudaStreamWaitEvent(ds, evDone[b], 0), "wait block");
+        cuda_check(cudaMemcpyAsync(C + j0 * e.m, plan->dC + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
+                                   cudaMemcpyDeviceToHost, ds),
+                   "D2H C block");
+    };
+    std::vector<char> have_a(static_cast<std::size_t>(nq), 0);
+    std::vector<int> finished;  // blocks whose D2H is issued one unit later (a pageable D2H blocks the host)
+    std::vector<std::pair<int, int>> units;
+    for (int wave = 0; wave < nbk + nq - 1; ++wave)
+        for (int b = std::max(0, wave - nq + 1); b <= std::min(nbk - 1, wave); ++b) units.push_back({b, wave - b});
+    {
+        for (auto [b, q] : units) {
+            const i64 j0 = ncut[static_cast<std::size_t>(b)], w = ncut[static_cast<std::size_t>(b) + 1] - j0;
+            const i64 p0 = kcut[static_cast<std::size_t>(q)], kq = kcut[static_cast<std::size_t>(q) + 1] - p0;
+            if (q == 0) {
+                cuda_check(cudaMemcpyAsync(plan->dC + j0 * e.m, C + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
+                                           cudaMemcpyHostToDevice, cs),
+                           "H2D C block");
+                cuda_check(cudaEventRecord(evC[b], cs), "event");
+            }
+            if (!have_a[static_cast<std::size_t>(q)]) {
+                have_a[static_cast<std::size_t>(q)] = 1;
+                cuda_check(cudaMemcpyAsync(plan->dA + p0 * e.m, A + p0 * e.m,
+                                           static_cast<std::size_t>(kq * e.m) * 8, cudaMemcpyHostToDevice, cs),
+                           "H2D A chunk");
+                cuda_check(cudaEventRecord(evA[q], cs), "event");
+            }
+            cuda_check(cudaMemcpy2DAsync(plan->dB + p0 + j0 * e.k, ld, B + p0 + j0 * e.k, ld,
+                                         static_cast<std::size_t>(kq) * 8, static_cast<std::size_t>(w),
+                                         cudaMemcpyHostToDevice, cs),
+                       "H2D B piece");
+            cudaEvent_t eb = evB[b * nq + q];
+            cuda_check(cudaEventRecord(eb, cs), "event");
+            // issue the GEMM right away so pageable-memory copies (which
+            // block the host while staging) still overlap device compute
+            if (q == 0) cuda_check(cudaStreamWaitEvent(st, evC[b], 0), "wait C block");
+            cuda_check(cudaStreamWaitEvent(st, evA[q], 0), "wait A chunk");
+            cuda_check(cudaStreamWaitEvent(st, eb, 0), "wait B piece");
+            tm_plan* pq = sub(w, kq);
+            run(pq, plan->dA + p0 * e.m, e.m, plan->dB + p0 + j0 * e.k, e.k, plan->dC + j0 * e.m, e.m, &o, st);
+            tasks += pq->last_tasks;
+            launches += pq->last_launches;
+            ctas = pq->last_ctas;
+            for (int f : finished) d2h(f);
+            finished.clear();
+            if (q == nq - 1) {
+                cuda_check(cudaEventRecord(evDone[b], st), "event");
+                finished.push_back(b);
+            }
+        }
+    }
+    for (int f : finished) d2h(f);
+    cuda_check(cudaStreamSynchronize(ds), "execute_host sync");
+    cuda_check(cudaStreamSynchronize(st), "execute_host sync");
+    plan->last_tasks = tasks;
+    plan->last_launches = launches;
+    plan->last_ctas = ctas;
+}
+
+}  // namespace engine
+}  // namespace mmm

@@ -1,0 +1,413 @@
+// Lowering of a loop nest onto CTA tasks and its execution on device
+// buffers (the blocked-loop driver, reference plan.hpp:61-84 +
+// exec.hpp:94-138, re-targeted): a task is one C region x k range run by one
+// CTA with its accumulators in registers. Two schedules:
+//   fused    — every k loop of the nest is sunk below its m/n loops, so each
+//              register-level C block is visited once, in the order of its
+//              first appearance in the nest (the m/n loops above it become the
+//              CTA raster: the L2-level plan sets which tiles share a wave).
+//              Optional split-k, finished in a fixed slot order.
+//   faithful — one task per nest cell, in nest order; cells of the same C
+//              block run in ascending k (per-region progress counters), so
+//              the C block round-trips to memory per cell exactly as the
+//              reference's micro-kernel does.
+// Either way every C entry is accumulated in ascending k from its incoming
+// value, which is what makes the result independent of the schedule.
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <unordered_map>
+
+#include "engine.hpp"
+
+namespace mmm {
+namespace engine {
+
+namespace {
+template <typename F>
+void for_each_subtile(i64 i0, i64 m, i64 j0, i64 n, int tm, int tn, F&& f) {
+    for (i64 jj = 0; jj < n; jj += tn)
+        for (i64 ii = 0; ii < m; ii += tm) f(i0 + ii, std::min<i64>(tm, m - ii), j0 + jj, std::min<i64>(tn, n - jj));
+}
+
+void check_i32(i64 v, const char* what) {
+    if (v > INT32_MAX) fail_usage(std::string(what) + " exceeds the 32-bit task range");
+}
+
+// Workspace slots and self-resetting counters of the in-kernel fix-up.
+void alloc_fixup(Schedule& s, const gpu::KernelInfo& info, int32_t slots, int32_t counters, cudaStream_t stream) {
+    if (counters == 0) return;
+    s.work_ld = info.tile_m;
+    s.work_slice = static_cast<i64>(info.tile_m) * info.tile_n;
+    cuda_check(cudaMalloc(&s.work, sizeof(double) * static_cast<std::size_t>(s.work_slice) * slots),
+               "cudaMalloc(split-k workspace)");
+    cuda_check(cudaMalloc(&s.progress, sizeof(int32_t) * static_cast<std::size_t>(counters)), "cudaMalloc(fix-up counters)");
+    cuda_check(cudaMemsetAsync(s.progress, 0, sizeof(int32_t) * static_cast<std::size_t>(counters), stream),
+               "zero fix-up counters");
+    s.counters = counters;
+}
+
+}  // namespace
+
+int sm_count() {
+    int dev = 0, sms = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    return sms;
+}
+
+gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o) {
+    const bool small_tile = o.tile == 64 || (o.tile == 0 && (nest.m_r < 128 || nest.n_r < 128));
+    if (o.tile != 0 && o.tile != 64 && o.tile != 128) fail_usage("tile must be 0, 64 or 128");
+    const int tn = o.tile_n == 0 ? o.tile : o.tile_n;
+    if (o.tile_n != 0 && !((o.tile == 128 && (tn == 64 || tn == 128)) || (o.tile == 64 && tn == 64)))
+        fail_usage("tile x tile_n must be 128x128, 128x64 or 64x64");
+    switch (o.numerics) {
+        case TM_NUMERICS_DMMA:
+            if (o.tile == 128 && tn == 64) return gpu::kDmma128x64;
+            // short k: every task is mostly C load/store; two CTAs per SM
+            // (128 x 64 tiles) hide one CTA's C traffic behind the other's DMMAs
+            if (o.tile == 0 && !small_tile && nest.ext.k <= 512 && o.schedule == TM_SCHEDULE_FUSED)
+                return gpu::kDmma128x64;
+            return small_tile ? gpu::kDmma64 : gpu::kDmma128;
+        case TM_NUMERICS_FMA:
+            if (tn == 64 && o.tile == 128) fail_usage("fma numerics run on square tiles");
+            return small_tile ? gpu::kFma64 : gpu::kFma128;
+        case TM_NUMERICS_EXACT:
+            if (o.tile == 128) fail_usage("exact numerics run on the 64x64 tile only");
+            return gpu::kExact64;
+        default: fail_usage("unknown numerics");
+    }
+}
+
+// Splits one C region into kernel tiles, n outer / m inner (the register
+// plan's own loop order, C0 = n then m).
+std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, cudaStream_t stream,
+                                bool upload) {
+    auto s = std::make_unique<Schedule>();
+    s->kernel = kernel;
+    gpu::KernelInfo info{};
+    const bool pair = kernel == gpu::kTc2Bf16 || kernel == gpu::kTc2Tf32;
+    if (kernel == gpu::kTcBf16 || kernel == gpu::kTcTf32)
+        info = gpu::KernelInfo{128, 256, 256, gpu::tc_smem_bytes(kernel == gpu::kTcTf32), 1};
+    else if (pair)
+        info = gpu::KernelInfo{256, 256, 256, gpu::tc2_smem_bytes(kernel == gpu::kTc2Tf32), 1};
+    else
+        cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
+    const int slots = sm_count() * std::max(1, info.ctas_per_sm);
+    const Extents& e = nest.ext;
+    check_i32(e.m, "m");
+    check_i32(e.n, "n");
+    check_i32(e.k, "k");
+    auto& T = s->host_tasks;
+
+    if (o.schedule == TM_SCHEDULE_FUSED) {
+        // First-appearance order of the register-level C blocks = the walk of
+        // the nest with its k loops removed.
+        Nest mn = nest;
+        mn.loops.clear();
+        for (const auto& L : nest.loops)
+            if (L.dim != kK) mn.loops.push_back(L);
+        std::vector<std::array<i64, 4>> tiles;
+        mn.walk([&](const Cell& c) {
+            for_each_subtile(c.i0, c.m, c.j0, c.n, info.tile_m, info.tile_n,
+                             [&](i64 i0, i64 m, i64 j0, i64 n) { tiles.push_back({i0, m, j0, n}); });
+        });
+        const bool dmma = o.numerics == TM_NUMERICS_DMMA && kernel < gpu::kTcBf16;
+        const i64 ntiles = static_cast<i64>(tiles.size());
+        // Stream-K (split_k == -1, or auto when C fills only a few waves with
+        // a ragged last one): every CTA gets an equal contiguous range of
+        // (tile, 32-deep k-slab) iterations; a tile cut by a range boundary
+        // becomes several k-parts reduced in fixed slot order afterwards.
+        // Balances the machine exactly and staggers the tile boundaries
+        // (C loads/stores) of different CTAs in time.
+        const bool ragged = ntiles % slots != 0 && ntiles < 8 * slots && ntiles * 2 > slots;
+        if (dmma && (o.split_k == -1 || (o.split_k == 0 && ragged && e.k >= 2048))) {
+            const i64 slab = 32, nks = cdiv(e.k, slab), U = ntiles * nks;
+            const int G = static_cast<int>(std::min<i64>(slots, U));
+            std::vector<std::vector<std::array<i64, 2>>> pieces(tiles.size());  // per tile: (slab_lo, slab_hi)
+            std::vector<std::vector<std::pair<i64, i64>>> per_cta(static_cast<std::size_t>(G));  // (tile, piece#)
+            for (int c = 0; c < G; ++c) {
+                const i64 lo = U * c / G, hi = U * (c + 1) / G;
+                for (i64 u = lo; u < hi;) {
+                    const i64 tile = u / nks, end = std::min(hi, (tile + 1) * nks);
+                    auto& pc = pieces[static_cast<std::size_t>(tile)];
+                    per_cta[static_cast<std::size_t>(c)].push_back({tile, static_cast<i64>(pc.size())});
+                    pc.push_back({u - tile * nks, end - tile * nks});
+                    u = end;
+                }
+            }
+            // A cut tile is finished inside the kernel: its head piece (k from
+            // 0, from C) is the owner and runs last in its CTA's range; the
+            // later pieces run first in the following CTAs' ranges and leave
+            // partials in slots slot0 .. slot0+pieces-2 (Task::fixup).
+            // Kernels built without the fix-up keep one slot per piece and a
+            // fixed-order reduce launch afterwards.
+            const bool fixk = kernel == gpu::kDmma128 || kernel == gpu::kDmma64;
+            std::vector<int32_t> slot0(tiles.size(), -1), counter(tiles.size(), -1);
+            std::vector<gpu::ReduceTile> red;
+            int32_t next_slot = 0, ncounters = 0;
+            for (std::size_t t = 0; t < tiles.size(); ++t)
+                if (pieces[t].size() > 1) {
+                    const int32_t np = static_cast<int32_t>(pieces[t].size());
+                    slot0[t] = next_slot;
+                    counter[t] = ncounters++;
+                    if (!fixk)
+                        red.push_back(gpu::ReduceTile{static_cast<int32_t>(tiles[t][0]), static_cast<int32_t>(tiles[t][2]),
+                                                      static_cast<int32_t>(tiles[t][1]), static_cast<int32_t>(tiles[t][3]),
+                                                      next_slot, np});
+                    next_slot += fixk ? np - 1 : np;
+                }
+            std::vector<int32_t> first(static_cast<std::size_t>(G) + 1, 0);
+            for (int c = 0; c < G; ++c) {
+                first[static_cast<std::size_t>(c)] = static_cast<int32_t>(T.size());
+                for (auto [tile, pi] : per_cta[static_cast<std::size_t>(c)]) {
+                    const auto& t = tiles[static_cast<std::size_t>(tile)];
+                    const auto& pr = pieces[static_cast<std::size_t>(tile)][static_cast<std::size_t>(pi)];
+                    gpu::Task tk{};
+                    tk.i0 = static_cast<int32_t>(t[0]);
+                    tk.m = static_cast<int32_t>(t[1]);
+                    tk.j0 = static_cast<int32_t>(t[2]);
+                    tk.n = static_cast<int32_t>(t[3]);
+                    tk.p0 = static_cast<int32_t>(pr[0] * slab);
+                    tk.k = static_cast<int32_t>(std::min(pr[1] * slab, e.k) - pr[0] * slab);
+                    const int32_t s0 = slot0[static_cast<std::size_t>(tile)];
+                    const int32_t np = static_cast<int32_t>(pieces[static_cast<std::size_t>(tile)].size());
+                    tk.tile = s0 < 0 ? -1 : -2 - counter[static_cast<std::size_t>(tile)];
+                    tk.from_c = pr[0] == 0 ? 1 : 0;
+                    if (s0 < 0) {
+                        tk.seq = 0;
+                        tk.slice = -1;
+                        tk.fixup = 0;
+                    } else if (!fixk) {  // every piece into its slot; the reduce launch sums them
+                        tk.tile = -1;
+                        tk.seq = 0;
+                        tk.slice = s0 + static_cast<int32_t>(pi);
+                        tk.fixup = 0;
+                    } else if (pi == 0) {  // owner
+                        tk.seq = np - 1;
+                        tk.slice = s0;
+                        tk.fixup = 2;
+                    } else {
+                        tk.seq = 0;
+                        tk.slice = s0 + static_cast<int32_t>(pi) - 1;
+                        tk.fixup = 1;
+                    }
+                    T.push_back(tk);
+                }
+            }
+            first[static_cast<std::size_t>(G)] = static_cast<int32_t>(T.size());
+            s->blocked = true;
+            s->grid_fixed = G;
+            cuda_check(cudaMalloc(&s->cta_first, sizeof(int32_t) * first.size()), "cudaMalloc(cta ranges)");
+            cuda_check(cudaMemcpyAsync(s->cta_first, first.data(), sizeof(int32_t) * first.size(),
+                                       cudaMemcpyHostToDevice, stream),
+                       "upload cta ranges");
+            if (fixk) {
+                alloc_fixup(*s, info, next_slot, ncounters, stream);
+            } else if (!red.empty()) {
+                s->slices = static_cast<int>(red.size());
+                s->work_ld = info.tile_m;
+                s->work_slice = static_cast<i64>(info.tile_m) * info.tile_n;
+                cuda_check(cudaMalloc(&s->work, sizeof(double) * static_cast<std::size_t>(s->work_slice) * next_slot),
+                           "cudaMalloc(stream-k workspace)");
+                cuda_check(cudaMalloc(&s->reduce, sizeof(gpu::ReduceTile) * red.size()), "cudaMalloc(reduce list)");
+                cuda_check(cudaMemcpyAsync(s->reduce, red.data(), sizeof(gpu::ReduceTile) * red.size(),
+                                           cudaMemcpyHostToDevice, stream),
+                           "upload reduce list");
+            }
+            cuda_check(cudaStreamSynchronize(stream), "upload stream-k lists (sync)");
+        } else {
+        // k parts per tile. split_k > 1: every tile; split_k == 0 (auto):
+        // every tile when C has too few tiles to fill the machine, otherwise
+        // only the tiles of the last, partial wave (a "tail split": the full
+        // waves run unsplit, the tail's parts fill the idle SMs).
+        const i64 slab = (kernel >= gpu::kTcBf16) ? 64 : 32;
+        const i64 nt = static_cast<i64>(tiles.size());
+        const i64 max_parts = std::max<i64>(1, std::min<i64>(8, e.k / (16 * slab)));
+        std::vector<int> parts(tiles.size(), 1);
+        if (o.split_k > 1) {
+            std::fill(parts.begin(), parts.end(), static_cast<int>(std::min<i64>(o.split_k, cdiv(e.k, slab))));
+        } else if (o.split_k == 0 && nt > 0 && o.numerics == TM_NUMERICS_DMMA) {
+            // (auto-splitting changes the summation order, so it is only
+            // applied where results are bound-checked, never for the
+            // bit-reproducible fma/exact numerics)
+            if (nt * 2 <= slots) {
+                const int sp = static_cast<int>(std::min<i64>(slots / nt, std::max<i64>(1, e.k / 1024)));
+                std::fill(parts.begin(), parts.end(), std::max(1, std::min<int>(sp, static_cast<int>(cdiv(e.k, slab)))));
+            } else {
+                const i64 full = (nt / slots) * slots, rem = nt - full;
+                // tail time in tile units: ceil(rem*S/slots)/S, plus a small
+                // charge per extra part for its partial store and reduction
+                double best = 1.0;
+                int bestS = 1;
+                for (i64 S = 2; S <= max_parts && rem > 0; ++S) {
+                    const double cost = static_cast<double>(cdiv(rem * S, slots)) / static_cast<double>(S) +
+                                        0.03 * static_cast<double>(S - 1);
+                    if (cost < best - 1e-9) {
+                        best = cost;
+                        bestS = static_cast<int>(S);
+                    }
+                }
+                for (i64 i = full; i < nt; ++i) parts[static_cast<std::size_t>(i)] = bestS;
+            }
+        }
+        // DMMA kernels finish split tiles in-kernel (Task::fixup): the owner
+        // part (k from 0, from C) is listed after its contributors, so every
+        // wait points at an earlier task of the persistent grid (no cycle).
+        // (the 128x64 short-k kernel is built without the fix-up: its register
+        // budget is two CTAs per SM; its few tail splits use the reduce launch)
+        const bool fix = kernel == gpu::kDmma128 || kernel == gpu::kDmma64;
+        int32_t next_slot = 0, ncounters = 0;
+        std::vector<gpu::ReduceTile> red;
+        for (std::size_t ti = 0; ti < tiles.size(); ++ti) {
+            const auto& t = tiles[ti];
+            const i64 per = cdiv(cdiv(e.k, parts[ti]), slab) * slab;
+            const int used = static_cast<int>(cdiv(e.k, per));
+            gpu::Task tk{};
+            tk.i0 = static_cast<int32_t>(t[0]);
+            tk.m = static_cast<int32_t>(t[1]);
+            tk.j0 = static_cast<int32_t>(t[2]);
+            tk.n = static_cast<int32_t>(t[3]);
+            tk.tile = -1;
+            tk.seq = 0;
+            if (used == 1) {
+                tk.p0 = 0;
+                tk.k = static_cast<int32_t>(e.k);
+                tk.slice = -1;
+                tk.from_c = 1;
+                T.push_back(tk);
+                continue;
+            }
+            if (fix) {
+                const int32_t ctr = ncounters++;
+                for (int q = 1; q <= used; ++q) {
+                    const int part = q % used;  // contributors 1..used-1, then the owner (part 0)
+                    const i64 p0 = part * per;
+                    tk.p0 = static_cast<int32_t>(p0);
+                    tk.k = static_cast<int32_t>(std::min(per, e.k - p0));
+                    tk.tile = -2 - ctr;
+                    tk.from_c = part == 0 ? 1 : 0;
+                    tk.fixup = part == 0 ? 2 : 1;
+                    tk.seq = part == 0 ? used - 1 : 0;
+                    tk.slice = part == 0 ? next_slot : next_slot + part - 1;
+                    T.push_back(tk);
+                }
+                next_slot += used - 1;
+                continue;
+            }
+            red.push_back(gpu::ReduceTile{tk.i0, tk.j0, tk.m, tk.n, next_slot, used});
+            for (int q = 0; q < used; ++q) {
+                const i64 p0 = q * per;
+                tk.p0 = static_cast<int32_t>(p0);
+                tk.k = static_cast<int32_t>(std::min(per, e.k - p0));
+                tk.slice = next_slot + q;
+                tk.from_c = q == 0 ? 1 : 0;
+                T.push_back(tk);
+            }
+            next_slot += used;
+        }
+        if (fix) alloc_fixup(*s, info, next_slot, ncounters, stream);
+        s->slices = static_cast<int>(red.size());
+        if (!red.empty()) {
+            s->work_ld = info.tile_m;
+            s->work_slice = static_cast<i64>(info.tile_m) * info.tile_n;
+            cuda_check(cudaMalloc(&s->work, sizeof(double) * static_cast<std::size_t>(s->work_slice) * next_slot),
+                       "cudaMalloc(split-k workspace)");
+            cuda_check(cudaMalloc(&s->reduce, sizeof(gpu::ReduceTile) * red.size()), "cudaMalloc(reduce list)");
+            cuda_check(cudaMemcpyAsync(s->reduce, red.data(), sizeof(gpu::ReduceTile) * red.size(),
+                                       cudaMemcpyHostToDevice, stream),
+                       "upload reduce list");
+            cuda_check(cudaStreamSynchronize(stream), "upload reduce list (sync)");
+        }
+        }  // uniform / tail split
+    } else if (o.schedule == TM_SCHEDULE_FAITHFUL) {
+        const i64 cells = nest.cells();
+        if (cells > 64LL * 1000 * 1000) fail_usage("faithful schedule limited to 64M cells; use the fused schedule");
+        std::unordered_map<i64, std::pair<int32_t, int32_t>> regions;  // key -> (id, next seq)
+        nest.walk([&](const Cell& c) {
+            for_each_subtile(c.i0, c.m, c.j0, c.n, info.tile_m, info.tile_n, [&](i64 i0, i64 m, i64 j0, i64 n) {
+                const i64 key = i0 * (e.n + 1) + j0;
+                auto it = regions.find(key);
+                if (it == regions.end()) it = regions.emplace(key, std::make_pair(static_cast<int32_t>(regions.size()), 0)).first;
+                gpu::Task tk{};
+                tk.i0 = static_cast<int32_t>(i0);
+                tk.m = static_cast<int32_t>(m);
+                tk.j0 = static_cast<int32_t>(j0);
+                tk.n = static_cast<int32_t>(n);
+                tk.p0 = static_cast<int32_t>(c.p0);
+                tk.k = static_cast<int32_t>(c.k);
+                tk.tile = it->second.first;
+                tk.seq = it->second.second++;
+                tk.slice = -1;
+                tk.from_c = 1;
+                T.push_back(tk);
+            });
+        });
+        s->regions = static_cast<int>(regions.size());
+        cuda_check(cudaMalloc(&s->progress, sizeof(int32_t) * static_cast<std::size_t>(std::max(1, s->regions))),
+                   "cudaMalloc(progress)");
+    } else {
+        fail_usage("unknown schedule");
+    }
+    if (T.size() > static_cast<std::size_t>(INT32_MAX)) fail_usage("too many tasks");
+    if (!upload) return s;  // host task list only (callers that splice task lists)
+    // Persistent grid: every CTA must be co-resident for the faithful
+    // schedule's waits to make progress.
+    int grid = o.ctas > 0 ? std::min(o.ctas, slots) : slots;
+    s->grid = std::max(1, std::min<int>(grid, static_cast<int>(T.size())));
+    if (pair) s->grid = 2 * std::max(1, std::min<int>(slots / 2, static_cast<int>(T.size())));  // clusters of 2
+    if (s->blocked) s->grid = s->grid_fixed;  // one task range per CTA
+    cuda_check(cudaGetDevice(&s->device), "cudaGetDevice");
+    cuda_check(cudaMalloc(&s->tasks, sizeof(gpu::Task) * std::max<std::size_t>(1, T.size())), "cudaMalloc(tasks)");
+    // Stream-ordered upload, completed before the schedule is used: a plain
+    // cudaMemcpy from pageable memory may return before the DMA lands, and the
+    // launch streams are non-blocking (no ordering with the legacy stream).
+    cuda_check(cudaMemcpyAsync(s->tasks, T.data(), sizeof(gpu::Task) * T.size(), cudaMemcpyHostToDevice, stream),
+               "upload tasks");
+    cuda_check(cudaStreamSynchronize(stream), "upload tasks (sync)");
+    return s;
+}
+
+bool origins_even(const std::vector<gpu::Task>& T) {
+    for (const auto& t : T)
+        if ((t.i0 | t.p0) & 1) return false;
+    return true;
+}
+
+void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+         const tm_exec_opts* opts, cudaStream_t stream) {
+    const Extents& e = plan->nest.ext;
+    if (!A || !B || !C) fail_usage("null operand pointer");
+    if (lda < e.m || ldb < e.k || ldc < e.m) fail_usage("leading dimension smaller than the operand's row count");
+    tm_exec_opts o{};
+    if (opts) o = *opts;
+    const gpu::Kernel kernel = pick_kernel(plan->nest, o);
+    std::lock_guard<std::mutex> lk(plan->mu);
+    Key key{o.schedule, kernel, o.schedule == TM_SCHEDULE_FUSED ? o.split_k : 0, o.ctas, false};
+    auto& slot = plan->schedules[key];
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (!slot || slot->device != dev) slot = lower(plan->nest, o, kernel, stream);
+    Schedule& s = *slot;
+    const bool vec16 = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(B) % 16 == 0) && origins_even(s.host_tasks);
+    if (s.regions > 0)
+        cuda_check(cudaMemsetAsync(s.progress, 0, sizeof(int32_t) * static_cast<std::size_t>(s.regions), stream),
+                   "reset progress");
+    gpu::Args a{A, lda, B, ldb, C, ldc, s.tasks, static_cast<int32_t>(s.host_tasks.size()), s.progress, s.work,
+                s.work_ld, s.work_slice, s.blocked ? s.cta_first : nullptr};
+    cuda_check(gpu::launch(s.kernel, vec16, a, s.grid, stream), "task kernel launch");
+    int launches = 1;
+    if (s.slices > 0) {
+        cuda_check(gpu::launch_reduce_tiles(C, ldc, s.work, s.work_ld, s.work_slice, s.reduce, s.slices, stream),
+                   "split-k reduce launch");
+        ++launches;
+    }
+    plan->last_tasks = static_cast<int64_t>(s.host_tasks.size());
+    plan->last_launches = launches;
+    plan->last_ctas = s.grid;
+}
+
+}  // namespace engine
+}  // namespace mmm
