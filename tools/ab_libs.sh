@@ -1,6 +1,6 @@
 for v in "$@"; do
   echo "== $v"
-  TILEMUL_B200_LIB=$PWD/exp_libs/$v.so python tools/sweep.py --tiles auto --members C2A1C0 --only ${ONLY:-config1,config3a_rank_k,config3c_panel_panel} 2>/dev/null | python -c "
+  TILEMUL_B200_LIB=$PWD/exp_libs/$v.so timeout 300 python tools/sweep.py --tiles auto --members C2A1C0 --only ${ONLY:-config1,config3a_rank_k,config3c_panel_panel} 2>/dev/null | python -c "
 import json,sys
 for l in sys.stdin:
     d=json.loads(l)
