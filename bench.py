@@ -41,6 +41,11 @@ sys.path.insert(0, ROOT)
 
 M = N = K = 16384
 FAMILY = "C2A1C0"
+METRIC = "GEMM TFLOP/s (FP64) and % of FP64 peak"  # both arms report this metric on this workload
+
+
+def workload_name(m):
+    return f"fp64 C+=A*B m=n=k={m} column-major, family {FAMILY} fused/DMMA"
 CPU_SAMPLE = (2048, 2048, 8192)      # bounded sub-problem of the same workload for the CPU reference
 CPU_SAMPLE_REF_ARM = (2048, 2048, 4096)
 
@@ -198,10 +203,10 @@ def reference_arm(args):
     sample = (f"reference execute() {FAMILY} on the {shape[0]}x{shape[1]}x{shape[2]} sub-problem of the "
               f"{M}^3 workload per step, host-derived blocksizes {sorted(bs.items())}, -O2 reference build")
     print(json.dumps({
-        "impl": "reference", "metric": "GEMM TFLOP/s (FP64)", "value": value, "unit": "TFLOP/s",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"fp64 C+=A*B m=n=k={M} column-major, family {FAMILY}", "sample": list(shape)},
+        "config": {"workload": workload_name(args.size), "sample": list(shape)},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": workers, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -275,7 +280,7 @@ def our_arm(args):
     achieved = flops / (kernel_ms * 1e-3) / 1e12
 
     peak = T.measure_fp64_peak(30)
-    workload = f"fp64 C+=A*B m=n=k={m} column-major, family {FAMILY} fused/DMMA"
+    workload = workload_name(m)
     traffic, traffic_src = ncu_traffic(workload)
     model = nest.model()
     hbm_model_bytes = model.at_level(hier.top_level()).total_bytes()
@@ -312,7 +317,7 @@ def our_arm(args):
                    "sample": f"unavailable: {exc}"}
 
     out = {
-        "metric": "GEMM TFLOP/s (FP64) and % of FP64 peak",
+        "metric": METRIC,
         "value": value, "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded counter-based uniform[-1,1) on device)",

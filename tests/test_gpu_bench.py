@@ -43,7 +43,11 @@ def test_bench_line_ours():
 
 def test_bench_line_reference_arm():
     d = run_bench("--impl", "reference", "--steps", "1", "--warmup", "3")
+    ours = run_bench("--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e")
     assert d["impl"] == "reference"
+    # the driver computes the ratio of the two lines: same metric, unit and workload
+    assert (d["metric"], d["unit"], d["higher_is_better"]) == (ours["metric"], ours["unit"], ours["higher_is_better"])
+    assert d["config"]["workload"] == ours["config"]["workload"]
     assert d["value"] > 0 and d["unit"] == "TFLOP/s"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
