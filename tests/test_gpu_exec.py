@@ -401,3 +401,38 @@ def test_randomized_split_modes_and_tiles():
                 ok, worst = H.entrywise_ok(got[ii + jj * m], want, ab, k, c0=c[ii + jj * m])
                 assert ok, (trial, m, n, k, kw, worst)
                 assert np.array_equal(got, run_gpu(nest, a, b, c, **kw)), (trial, kw)
+
+
+def test_host_pipeline_fallback_under_launch_blocking():
+    """With CUDA_LAUNCH_BLOCKING=1 (or a profiler injected) the persistent,
+    copy-engine-fed pipeline cannot run (its tasks wait on another stream's
+    copies); tm_execute_host takes the one-launch-per-unit path instead, with
+    bitwise the same result."""
+    import subprocess
+    import sys
+
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+from paper_1904_05717_b200 import tilemul as T
+from oracle import oracle as O
+m, n, k = 520, 2200, 8224
+hier = T.gpu_hierarchy(128)
+d = T.parse_name('C2A1C0')
+bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(128, 128)),
+                         pinned=T.BlocksizeSet({(1, 'm'): 128}))
+nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+a, b, c = O.fill_uniform(31, [(m, k), (k, n), (m, n)])
+Cd = torch.from_numpy(c.copy()).cuda()
+T.execute(nest, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), Cd)
+torch.cuda.synchronize()
+hc = c.copy()
+T.execute(nest, a, b, hc)
+assert nest.last_launch()['launches'] > 1, nest.last_launch()
+assert np.array_equal(hc.view(np.uint64), Cd.cpu().numpy().view(np.uint64))
+print('ok')
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, CUDA_LAUNCH_BLOCKING="1"))
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
