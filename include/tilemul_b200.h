@@ -91,6 +91,11 @@ typedef struct {
     int32_t tile;       /* CTA tile rows: 128 or 64 (0 = auto from the register tile); tensor-core path:
                            128 = one SM (cta_group::1), 0/256 = an SM pair (cta_group::2) */
     int32_t tile_n;     /* CTA tile columns (0 = same as tile); 128 x 64 runs two CTAs per SM */
+    /* Faithful schedule: the m/n loop whose iterations run as independent
+     * workers (ExecOptions::parallel_loop, exec.hpp:50-53, :125-131), as
+     * loop index + 1; 0 = auto (the deepest m/n loop above the innermost k
+     * loop). A k loop is rejected (status 2), like the reference. */
+    int32_t parallel_loop;
 } tm_exec_opts;
 
 typedef struct tm_plan tm_plan;

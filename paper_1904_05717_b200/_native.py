@@ -37,7 +37,7 @@ class tm_derive_opts(C.Structure):
 
 class tm_exec_opts(C.Structure):
     _fields_ = [("numerics", C.c_int32), ("schedule", C.c_int32), ("split_k", C.c_int32), ("ctas", C.c_int32),
-                ("tile", C.c_int32), ("tile_n", C.c_int32)]
+                ("tile", C.c_int32), ("tile_n", C.c_int32), ("parallel_loop", C.c_int32)]
 
 
 class tm_sim_level(C.Structure):

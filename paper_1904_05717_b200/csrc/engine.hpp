@@ -53,8 +53,10 @@ struct Schedule {
 struct Key {
     int schedule, kernel, split, ctas;
     bool vec16;
+    int par;  // faithful: parallel loop (+1, 0 = auto)
     bool operator<(const Key& o) const {
-        return std::tie(schedule, kernel, split, ctas, vec16) < std::tie(o.schedule, o.kernel, o.split, o.ctas, o.vec16);
+        return std::tie(schedule, kernel, split, ctas, vec16, par) <
+               std::tie(o.schedule, o.kernel, o.split, o.ctas, o.vec16, o.par);
     }
 };
 

@@ -155,7 +155,7 @@ std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o,
 
 bool same_opts(const tm_exec_opts& a, const tm_exec_opts& b) {
     return a.numerics == b.numerics && a.schedule == b.schedule && a.split_k == b.split_k && a.ctas == b.ctas &&
-           a.tile == b.tile && a.tile_n == b.tile_n;
+           a.tile == b.tile && a.tile_n == b.tile_n && a.parallel_loop == b.parallel_loop;
 }
 
 void run_pipe(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts& o) {

@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <array>
 #include <cstring>
+#include <functional>
+#include <tuple>
 #include <unordered_map>
 
 #include "engine.hpp"
@@ -45,6 +47,28 @@ void alloc_fixup(Schedule& s, const gpu::KernelInfo& info, int32_t slots, int32_
     cuda_check(cudaMemsetAsync(s.progress, 0, sizeof(int32_t) * static_cast<std::size_t>(counters), stream),
                "zero fix-up counters");
     s.counters = counters;
+}
+
+// The nest walk (Nest::walk, plan.hpp:61-84) also reporting, per cell, the
+// iteration index of loop `par` at the visit that produced it (0 if par < 0).
+void walk_indexed_rec(const Nest& nest, std::size_t depth, int par, i64 widx, std::array<i64, 3> org,
+                      std::array<i64, 3> ext, const std::function<void(const Cell&, i64)>& f) {
+    if (depth == nest.loops.size()) {
+        f(Cell{org[0], ext[0], org[1], ext[1], org[2], ext[2]}, widx);
+        return;
+    }
+    const Loop& L = nest.loops[depth];
+    const int d = L.dim;
+    const i64 lo = org[d], hi = org[d] + ext[d];
+    i64 it = 0;
+    for (i64 s0 = lo; s0 < hi; s0 += L.size, ++it) {
+        org[d] = s0;
+        ext[d] = std::min(L.size, hi - s0);
+        walk_indexed_rec(nest, depth + 1, par, static_cast<int>(depth) == par ? it : widx, org, ext, f);
+    }
+}
+void walk_indexed(const Nest& nest, int par, const std::function<void(const Cell&, i64)>& f) {
+    walk_indexed_rec(nest, 0, par, 0, {0, 0, 0}, {nest.ext.m, nest.ext.n, nest.ext.k}, f);
 }
 
 }  // namespace
@@ -324,8 +348,29 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
     } else if (o.schedule == TM_SCHEDULE_FAITHFUL) {
         const i64 cells = nest.cells();
         if (cells > 64LL * 1000 * 1000) fail_usage("faithful schedule limited to 64M cells; use the fused schedule");
+        // The reference runs a chosen m/n loop's iterations on separate
+        // workers, each walking its share in nest order (plan.hpp:49-84,
+        // exec.hpp:106-131). Here every iteration of that loop is a worker and
+        // the workers' task lists are interleaved, so the CTAs in flight hold
+        // independent C regions; a region's cells keep their nest order
+        // (progress counters), and every wait points at an earlier task.
+        const int nl = static_cast<int>(nest.loops.size());
+        int par = o.parallel_loop - 1;
+        if (o.parallel_loop == 0) {  // auto: the deepest m/n loop above the innermost k loop
+            int kin = -1;
+            for (int d = 0; d < nl; ++d)
+                if (nest.loops[static_cast<std::size_t>(d)].dim == kK) kin = d;
+            for (int d = 0; d < kin; ++d)
+                if (nest.loops[static_cast<std::size_t>(d)].dim != kK) par = d;
+        } else {
+            if (par < 0 || par >= nl) fail_usage("parallel loop index out of range");
+            if (nest.loops[static_cast<std::size_t>(par)].dim == kK)
+                fail_usage("cannot parallelize a k-dimension loop: workers would accumulate into shared C");
+        }
+        std::vector<std::vector<gpu::Task>> workers(1);
         std::unordered_map<i64, std::pair<int32_t, int32_t>> regions;  // key -> (id, next seq)
-        nest.walk([&](const Cell& c) {
+        walk_indexed(nest, par, [&](const Cell& c, i64 w) {
+            if (static_cast<std::size_t>(w) >= workers.size()) workers.resize(static_cast<std::size_t>(w) + 1);
             for_each_subtile(c.i0, c.m, c.j0, c.n, info.tile_m, info.tile_n, [&](i64 i0, i64 m, i64 j0, i64 n) {
                 const i64 key = i0 * (e.n + 1) + j0;
                 auto it = regions.find(key);
@@ -341,9 +386,18 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
                 tk.seq = it->second.second++;
                 tk.slice = -1;
                 tk.from_c = 1;
-                T.push_back(tk);
+                workers[static_cast<std::size_t>(w)].push_back(tk);
             });
         });
+        // merge by relative position so unequal workers (margins) advance in
+        // proportion to their size: task r of a worker of n tasks sorts at
+        // (r + 1/2) / n
+        std::vector<std::tuple<double, std::size_t, std::size_t>> order;
+        for (std::size_t w = 0; w < workers.size(); ++w)
+            for (std::size_t r = 0; r < workers[w].size(); ++r)
+                order.emplace_back((static_cast<double>(r) + 0.5) / static_cast<double>(workers[w].size()), w, r);
+        std::sort(order.begin(), order.end());
+        for (const auto& [key, w, r] : order) T.push_back(workers[w][r]);
         s->regions = static_cast<int>(regions.size());
         cuda_check(cudaMalloc(&s->progress, sizeof(int32_t) * static_cast<std::size_t>(std::max(1, s->regions))),
                    "cudaMalloc(progress)");
@@ -384,7 +438,8 @@ void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t l
     if (opts) o = *opts;
     const gpu::Kernel kernel = pick_kernel(plan->nest, o);
     std::lock_guard<std::mutex> lk(plan->mu);
-    Key key{o.schedule, kernel, o.schedule == TM_SCHEDULE_FUSED ? o.split_k : 0, o.ctas, false};
+    Key key{o.schedule, kernel, o.schedule == TM_SCHEDULE_FUSED ? o.split_k : 0, o.ctas, false,
+            o.schedule == TM_SCHEDULE_FAITHFUL ? o.parallel_loop : 0};
     auto& slot = plan->schedules[key];
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");

@@ -436,3 +436,22 @@ print('ok')
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
                        env=dict(os.environ, CUDA_LAUNCH_BLOCKING="1"))
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
+# --- exec.hpp:106-131 / test_exec.cpp:223-254: the parallel loop never changes
+# results (faithful schedule: each iteration of the chosen m/n loop is a worker)
+def test_faithful_parallel_loop_choice_is_bitwise_invariant():
+    m, n, k = 300, 260, 530
+    d = T.parse_name("B2A1C0")
+    hier = T.gpu_hierarchy(64)
+    bs = T.BlocksizeSet({(2, "n"): 128, (2, "k"): 192, (1, "m"): 64, (1, "k"): 64, (0, "n"): 64, (0, "m"): 64})
+    nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+    a, b, c = O.fill_uniform(17, [(m, k), (k, n), (m, n)])
+    want = oracle_exec(nest, a, b, c)
+    outs = []
+    for par in (-1, 0, 2, 4, 5):  # auto, n2, m1, n0, m0 (k loops are at 1 and 3)
+        got = run_gpu(nest, a, b, c, numerics="exact", schedule="faithful", parallel_loop=par)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), par
+        outs.append(got)
+    with pytest.raises(ValueError):
+        run_gpu(nest, a, b, c, numerics="exact", schedule="faithful", parallel_loop=1)  # k2
