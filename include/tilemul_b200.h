@@ -93,8 +93,9 @@ typedef struct {
     int32_t tile_n;     /* CTA tile columns (0 = same as tile); 128 x 64 runs two CTAs per SM */
     /* Faithful schedule: the m/n loop whose iterations run as independent
      * workers (ExecOptions::parallel_loop, exec.hpp:50-53, :125-131), as
-     * loop index + 1; 0 = auto (the deepest m/n loop above the innermost k
-     * loop). A k loop is rejected (status 2), like the reference. */
+     * loop index + 1; 0 = plain nest order (consecutive cells on the CTAs,
+     * the member's own traffic). A k loop is rejected (status 2), like the
+     * reference. */
     int32_t parallel_loop;
 } tm_exec_opts;
 

@@ -354,14 +354,16 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
         // the workers' task lists are interleaved, so the CTAs in flight hold
         // independent C regions; a region's cells keep their nest order
         // (progress counters), and every wait points at an earlier task.
+        // Default: plain nest order (the CTAs take consecutive cells), which
+        // reproduces the member's traffic (0.95-1.03x its model, DESIGN.md
+        // 5.3). Naming an m/n loop splits its iterations into workers like the
+        // reference's threads: an outer one (e.g. m1 of B2A1C0) runs several
+        // resident blocks at once -- far more parallel, but their combined
+        // working set no longer matches the member's model.
         const int nl = static_cast<int>(nest.loops.size());
         int par = o.parallel_loop - 1;
-        if (o.parallel_loop == 0) {  // auto: the deepest m/n loop above the innermost k loop
-            int kin = -1;
-            for (int d = 0; d < nl; ++d)
-                if (nest.loops[static_cast<std::size_t>(d)].dim == kK) kin = d;
-            for (int d = 0; d < kin; ++d)
-                if (nest.loops[static_cast<std::size_t>(d)].dim != kK) par = d;
+        if (o.parallel_loop == 0) {
+            par = -1;
         } else {
             if (par < 0 || par >= nl) fail_usage("parallel loop index out of range");
             if (nest.loops[static_cast<std::size_t>(par)].dim == kK)

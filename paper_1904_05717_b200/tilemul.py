@@ -472,7 +472,7 @@ class ExecOptions:  # exec.hpp:48-53, re-targeted
     ctas: int = 0               # persistent grid (0 = SMs x occupancy)
     tile: int = 0               # CTA tile rows 64/128 (0 = from the register tile)
     tile_n: int = 0             # CTA tile columns (0 = tile); 128x64 runs two CTAs per SM
-    parallel_loop: int = -1     # faithful: loop whose iterations run as independent workers (-1 = auto)
+    parallel_loop: int = -1     # faithful: loop whose iterations run as independent workers (-1 = nest order)
 
     def _c(self):
         return N.tm_exec_opts(NUMERICS[self.numerics], SCHEDULES[self.schedule], self.split_k, self.ctas, self.tile,

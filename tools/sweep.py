@@ -74,6 +74,9 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--once", action="store_true")
     ap.add_argument("--schedules", default="fused")
+    ap.add_argument("--faithful-par", default="default", choices=["default", "outer"],
+                    help="faithful: plain nest order, or the deepest m/n loop above the innermost k loop split into "
+                         "workers (faster, not traffic-faithful)")
     ap.add_argument("--tiles", default="auto,128x128,128x64")
     ap.add_argument("--only", default="", help="comma-separated config names to run (default: all)")
     ap.add_argument("--members", default="", help="comma-separated family members (default: per config)")
@@ -114,8 +117,14 @@ def main():
                     C.zero_()
                 else:
                     T.fill_uniform_device(C, 3)
+                par = -1
+                if sched == "faithful" and a.faithful_par == "outer":
+                    dims = [L.dim for L in nest.loops]
+                    kin = max((i for i, d in enumerate(dims) if d == "k"), default=-1)
+                    par = max((i for i in range(kin) if dims[i] != "k"), default=-1)
+                    rec["parallel_loop"] = par
                 opts = T.ExecOptions(numerics="dmma", schedule=sched, split_k=extra.get("split_k", 0), tile=tm,
-                                     tile_n=tn)
+                                     tile_n=tn, parallel_loop=par)
                 rep = nest.model()
                 rec["blocksizes"] = {f"{lv}:{d}": v for (lv, d), v in bs.entries()}
                 rec["model_bytes"] = {f"L{lt.level}": lt.total_bytes() for lt in rep.levels}
