@@ -196,6 +196,12 @@ int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, 
 /* Sustained FP64 tensor-pipe (DMMA) rate of the current device in TFLOP/s,
  * from `launches` ~7 ms probe launches: the roofline denominator. */
 int tm_measure_fp64_peak(int launches, double* tflops);
+/* Peak tcgen05 MMA rate (M=128 x N=256, fp32 accumulate) for dtype
+ * TM_DTYPE_BF16 or TM_DTYPE_TF32, best of `launches` launches of ~5 ms
+ * (sustained = 0: full clocks) or ~200 ms (sustained != 0: under the power
+ * cap, like a long GEMM): the measured roofline denominator of the
+ * tensor-core path. */
+int tm_measure_tc_peak(int dtype, int launches, int sustained, double* tflops);
 
 /* The reference `run` command's inputs on the host (tools/tilemul_main.cpp:236-242):
  * mt19937_64(seed), uniform(-1,1), filling A, then B, then C (C may be NULL). */

@@ -90,6 +90,7 @@ SIGNATURES = [
     ("tm_plan_last_launch", C.c_int, [P, C.POINTER(i64), C.POINTER(i32), C.POINTER(i32)]),
     ("tm_fill_seeded", C.c_int, [C.c_uint64, P, i64, P, i64, P, i64]),
     ("tm_measure_fp64_peak", C.c_int, [C.c_int, C.POINTER(dbl)]),
+    ("tm_measure_tc_peak", C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(dbl)]),
     ("tm_fill_uniform_device", C.c_int, [P, i64, C.c_uint64, C.c_uint64, P]),
     ("tm_fill_uniform_block", C.c_int, [P, i64, i64, i64, C.c_uint64, i64, i64, i64, P]),
     ("tm_trace_event_count", i64, [P]),

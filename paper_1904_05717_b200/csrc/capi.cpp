@@ -424,6 +424,15 @@ int tm_measure_fp64_peak(int launches, double* tflops) {
     return guard([&] { cuda_check(gpu::measure_fp64_peak(launches < 1 ? 1 : launches, tflops), "fp64 peak probe"); });
 }
 
+int tm_measure_tc_peak(int dtype, int launches, int sustained, double* tflops) {
+    return guard([&] {
+        if (dtype != TM_DTYPE_BF16 && dtype != TM_DTYPE_TF32) fail_usage("dtype must be TM_DTYPE_BF16 or TM_DTYPE_TF32");
+        if (!tflops) fail_usage("null output");
+        cuda_check(gpu::measure_tc_peak(dtype == TM_DTYPE_TF32, launches < 1 ? 1 : launches, sustained != 0, tflops),
+                   "tensor-core peak probe");
+    });
+}
+
 int tm_fill_uniform_block(double* x, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, int64_t row0,
                           int64_t col0, int64_t global_ld, void* stream) {
     return guard([&] {

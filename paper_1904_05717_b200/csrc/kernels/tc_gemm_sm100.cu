@@ -1,3 +1,4 @@
+#include <algorithm>
 // BF16 / TF32-input C(fp32) += A·B on the 5th-generation tensor cores
 // (tcgen05 + TMEM), BASELINE.json configs[3]. sm_100a only.
 //
@@ -290,6 +291,86 @@ __global__ void __launch_bounds__(256, 1) k_tc(const __grid_constant__ CUtensorM
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem_base) : "memory");
     }
+}
+
+// ======================= tensor-pipe peak probe =======================
+// One CTA per SM, one thread issuing M=128 x N=256 tcgen05.mma back to back
+// from fixed shared-memory operands (contents irrelevant to throughput) into
+// one TMEM accumulator: the issue-rate ceiling of the MMA path the GEMM
+// kernels use, measured on this device under its own clocks and power cap.
+template <bool TF32>
+__global__ void __launch_bounds__(128, 1) k_tc_peak(int iters) {
+    using G = TcGeo<TF32>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* done = reinterpret_cast<uint64_t*>(smem + G::STAGE);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(saddr(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) {
+        constexpr uint32_t idesc = instr_desc<TF32>();
+        const uint32_t sa = saddr(smem), sb = sa + G::A_BYTES;
+        for (int i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int kk = 0; kk < G::NMMA; ++kk)
+                umma<TF32>(tmem, smem_desc(sa + kk * G::UK * 128, G::A_BOX_BYTES, G::A_SBO, G::A_LAYOUT),
+                           smem_desc(sb + kk * 32, 16, 1024), idesc, (i | kk) != 0 ? 1u : 0u);
+        }
+        umma_commit(done);
+        mbar_wait(done, 0);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem) : "memory");
+    }
+}
+
+template <bool TF32>
+cudaError_t measure_tc_peak_t(int launches, bool sustained, double* tflops) {
+    using G = TcGeo<TF32>;
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // ~half the opt-in shared memory: one CTA per SM
+    const int smem = 110 * 1024;
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_tc_peak<TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    // ~5 ms per launch (burst: full clocks), or ~200 ms (sustained: under the power cap, like a long GEMM)
+    const int iters = (TF32 ? 2048 : 4096) * (sustained ? 40 : 1);
+    const double flops = 2.0 * kTcBM * kTcBN * G::BK * static_cast<double>(iters) * sms;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_tc_peak<TF32><<<sms, 128, smem>>>(iters);  // warm-up
+    double best = 0;
+    for (int l = 0; l < launches && e == cudaSuccess; ++l) {
+        cudaEventRecord(e0);
+        k_tc_peak<TF32><<<sms, 128, smem>>>(iters);
+        cudaEventRecord(e1);
+        e = cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *tflops = best;
+    return e;
 }
 
 // ======================= 2-SM pair kernel (cta_group::2) =======================
@@ -665,6 +746,11 @@ cudaError_t launch_round(bool tf32, const double* x, void* y, int64_t count, cud
 }
 
 int tc_smem_bytes(bool tf32) { return tf32 ? TcGeo<true>::SMEM : TcGeo<false>::SMEM; }
+
+cudaError_t measure_tc_peak(bool tf32, int launches, bool sustained, double* tflops) {
+    return tf32 ? measure_tc_peak_t<true>(launches, sustained, tflops)
+                : measure_tc_peak_t<false>(launches, sustained, tflops);
+}
 
 }  // namespace gpu
 }  // namespace mmm

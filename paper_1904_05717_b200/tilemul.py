@@ -711,6 +711,15 @@ def fill_uniform_block(x, rows: int, cols: int, ld: int, seed: int, row0: int, c
     _check(N.lib().tm_fill_uniform_block(x.data_ptr(), rows, cols, ld, seed, row0, col0, global_ld, C.c_void_p(st)))
 
 
+def measure_tc_peak(dtype: str = "bf16", launches: int = 10, sustained: bool = False) -> float:
+    """Peak tcgen05 MMA TFLOP/s of the current device for bf16 or tf32 inputs
+    (roofline denominator): ~5 ms bursts at full clocks, or ~200 ms launches
+    under the power cap (sustained=True)."""
+    v = C.c_double(0)
+    _check(N.lib().tm_measure_tc_peak(DTYPES[dtype], launches, int(sustained), C.byref(v)))
+    return v.value
+
+
 def measure_fp64_peak(launches: int = 20) -> float:
     """Sustained FP64 DMMA TFLOP/s of the current device (roofline denominator)."""
     v = C.c_double(0)

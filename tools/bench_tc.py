@@ -35,6 +35,9 @@ def main():
     B64 = torch.empty(k * n, dtype=torch.float64, device="cuda")
     T.fill_uniform_device(A64, 1)
     T.fill_uniform_device(B64, 2)
+    # live tcgen05 issue-rate peaks: bursts at full clocks, and ~200 ms launches under the power cap
+    probe = {dt: T.measure_tc_peak(dt, 10) for dt in ("bf16", "tf32")}
+    probe_sus = {dt: T.measure_tc_peak(dt, 3, sustained=True) for dt in ("bf16", "tf32")}
     for dtype, tile in (("bf16", 256), ("bf16", 128), ("tf32", 256), ("tf32", 128)):
         nest, bs = plan(tile)
         A = T.round_inputs(A64, dtype)
@@ -61,7 +64,10 @@ def main():
         print(json.dumps({"config": "config4", "dtype": dtype, "shape": [m, n, k], "seconds": t, "tflops": tf,
                           "peak_tflops": peak,
                           "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" + (" / 2 (nominal tf32:bf16 dense ratio)" if dtype == "tf32" else ""),
-                          "frac": tf / peak,
+                          "frac": tf / peak, "probe_peak_tflops": probe[dtype], "frac_of_probe": tf / probe[dtype],
+                          "probe_sustained_tflops": probe_sus[dtype], "frac_of_probe_sustained": tf / probe_sus[dtype],
+                          "probe_source": "tm_measure_tc_peak: one CTA per SM issuing 128x256 tcgen05.mma back to back "
+                                          "(cta_group::1), same clocks/power state as this run",
                           "frac_of_sustained": tf / (peaks.get("bf16_tflops_sustained", peak * 2) /
                                                     (1 if dtype == "bf16" else 2)),
                           "cta_tile": "256x256 per SM pair (cta_group::2)" if tile == 256 else "128x256 (cta_group::1)",
