@@ -716,7 +716,7 @@ def measure_tc_peak(dtype: str = "bf16", launches: int = 10, sustained: bool = F
     (roofline denominator): ~5 ms bursts at full clocks, or ~200 ms launches
     under the power cap (sustained=True)."""
     v = C.c_double(0)
-    _check(N.lib().tm_measure_tc_peak(DTYPES[dtype], launches, int(sustained), C.byref(v)))
+    _check(N.lib().tm_measure_tc_peak(DTYPES.get(dtype, 0), launches, int(sustained), C.byref(v)))
     return v.value
 
 

@@ -83,3 +83,14 @@ def test_tc_rejects_unaligned_and_faithful():
     nest = tc_plan(128, 256, 64)
     with pytest.raises(ValueError):
         T.execute_tc(nest, A[:128 * 64], B, C[:128 * 256], "bf16", T.ExecOptions(schedule="faithful"))
+
+
+def test_tc_peak_probe():
+    """tm_measure_tc_peak: the tcgen05 issue-rate ceiling (roofline denominator
+    of this path); tf32 runs at half the bf16 rate, as the instruction set says."""
+    bf16 = T.measure_tc_peak("bf16", 3)
+    tf32 = T.measure_tc_peak("tf32", 3)
+    assert bf16 > 1000.0
+    assert 0.4 < tf32 / bf16 < 0.6
+    with pytest.raises(ValueError):
+        T.measure_tc_peak("fp8", 1)
