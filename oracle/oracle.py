@@ -113,6 +113,8 @@ def ref():
                                                                C.c_char_p, C.c_int]
         L.ref_simulate.argtypes = [cp] + hier + bs + shier + [C.c_int, C.c_int, C.c_int, _i64p, C.POINTER(C.c_int),
                                                               C.POINTER(C.c_int64), C.c_char_p, C.c_int]
+        L.ref_pareto.argtypes = [C.c_int64, _dp, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_int64,
+                                 C.c_int64, _dp, C.c_char_p, C.c_int]
         L.ref_trace.argtypes = [cp] + hier + bs + [C.c_int, C.c_int64, C.c_char_p, _i64p,
                                                    np.ctypeslib.ndpointer(dtype=np.uint8), C.POINTER(C.c_int64),
                                                    C.c_char_p, C.c_int]
@@ -340,3 +342,15 @@ def ref_trace(name, caps, shape, bs, packed=False, cap=1 << 20):
         raise ValueError(err.value.decode())
     n = min(cap, cnt.value)
     return ops.raw[:n].decode(), idx[:n], wr[:n], cnt.value
+
+
+def ref_pareto(outer, ratios, shape, slack=1.0 / 16.0, mr=4, nr=12):
+    """The reference pareto_sweep -> list of 8-tuples (ParetoPoint fields), or ValueError."""
+    L = ref()
+    r = np.ascontiguousarray(ratios, dtype=np.float64)
+    out = np.zeros(8 * max(1, r.size), dtype=np.float64)
+    err = C.create_string_buffer(4096)
+    rc = L.ref_pareto(outer, r, r.size, *shape, slack, mr, nr, out, err, 4096)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    return [tuple(out[8 * i:8 * i + 8]) for i in range(r.size)]

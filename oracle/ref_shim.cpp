@@ -358,4 +358,24 @@ int ref_trace(const char* name, const int64_t* caps, const int* inclusive, int n
     });
 }
 
+// pareto_sweep (costmodel.hpp:299-328): 8 values per point, in ParetoPoint field order.
+int ref_pareto(int64_t outer, const double* ratios, int nratios, int64_t m, int64_t n, int64_t k, double slack,
+               int64_t mr, int64_t nr, double* out, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        DeriveOptions o;
+        o.slack = slack;
+        o.micro = MicroTile{mr, nr};
+        const auto pts = pareto_sweep(outer, std::vector<double>(ratios, ratios + nratios), Shape(m, n, k), o);
+        int i = 0;
+        for (const auto& p : pts) {
+            const double v[8] = {p.ratio, static_cast<double>(p.inner_capacity), static_cast<double>(p.outer_block_k),
+                                 static_cast<double>(p.outer_block_n), static_cast<double>(p.inner_block_m),
+                                 static_cast<double>(p.inner_block_k), p.eff_outer_flops_per_element,
+                                 p.eff_inner_flops_per_element};
+            for (int q = 0; q < 8; ++q) out[8 * i + q] = v[q];
+            ++i;
+        }
+    });
+}
+
 }  // extern "C"

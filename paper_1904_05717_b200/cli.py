@@ -1,6 +1,7 @@
 """Command-line surface on the GPU, mirroring the reference CLI's `run`,
-`analyze`, `simulate` and `plan` subcommands (/root/reference/proj/tools/
-tilemul_main.cpp:163-229, :231-304, :306-360): same flags where they apply,
+`analyze`, `simulate`, `plan`, `roofline` and `pareto` subcommands
+(/root/reference/proj/tools/tilemul_main.cpp:163-229, :231-304, :306-431):
+same flags where they apply,
 same JSON keys, same exit codes — 0 ok, 1 validation/parse/infeasible or a
 failed correctness check, 2 usage/config error (:519-535).
 
@@ -237,6 +238,56 @@ def cmd_simulate(a) -> int:  # tilemul_main.cpp:179-229 + serialize.hpp:174-235
     return 0
 
 
+def _num(x: float) -> str:  # std::ostream's default formatting (6 significant digits)
+    return f"{x:g}"
+
+
+def cmd_roofline(a) -> int:  # tilemul_main.cpp:355-388
+    rows, csv = [], ["name,intensity_flops_per_byte,bound_flops_per_s,regime"]
+    for p in a.point or []:
+        if "=" not in p:
+            raise ConfigError(f"bad --point '{p}', expected name=intensity")
+        name, val = p.split("=", 1)
+        try:
+            intensity = float(val)
+        except ValueError:
+            raise ConfigError(f"bad --point '{p}', expected name=intensity")
+        bound = T.roofline_bound(intensity, a.peak, a.bw)
+        regime = "compute-bound" if intensity * a.bw >= a.peak else "bandwidth-bound"
+        csv.append(f"{name},{_num(intensity)},{_num(bound)},{regime}")
+        rows.append({"name": name, "intensity_flops_per_byte": intensity, "bound_flops_per_s": bound, "regime": regime})
+    breakpoint_ = a.peak / a.bw
+    csv.append(f"_breakpoint,{_num(breakpoint_)},{_num(a.peak)},breakpoint")
+    if a.format == "json":
+        emit(a, json.dumps({"peak_flops_per_s": a.peak, "bandwidth_bytes_per_s": a.bw,
+                            "breakpoint_intensity": breakpoint_, "points": rows}, indent=2) + "\n")
+    else:
+        emit(a, "\n".join(csv) + "\n")
+    return 0
+
+
+def cmd_pareto(a) -> int:  # tilemul_main.cpp:390-431
+    shape = parse_shape(a.shape)
+    try:
+        ratios = [float(x) for x in a.ratios.split(",") if x]
+    except ValueError:
+        raise ConfigError(f"bad --ratios '{a.ratios}'")
+    if not ratios:
+        raise ConfigError("--ratios needs at least one value")
+    pts = T.pareto_sweep(a.cache, ratios, shape,
+                         T.DeriveOptions(a.slack, T.MicroTile(a.mr if a.mr else 4, a.nr if a.nr else 12)))
+    keys = ["ratio", "inner_capacity", "outer_block_k", "outer_block_n", "inner_block_m", "inner_block_k",
+            "eff_outer_flops_per_element", "eff_inner_flops_per_element"]
+    if a.format == "json":
+        emit(a, json.dumps({"outer_capacity": a.cache, "points": [{k: getattr(p, k) for k in keys} for p in pts]},
+                           indent=2) + "\n")
+    else:
+        lines = [",".join(keys)] + [",".join(_num(getattr(p, k)) if isinstance(getattr(p, k), float)
+                                             else str(getattr(p, k)) for k in keys) for p in pts]
+        emit(a, "\n".join(lines) + "\n")
+    return 0
+
+
 def cmd_plan(a) -> int:  # tilemul_main.cpp:306-360, re-targeted (planner.py)
     defaults(a)
     shape = parse_shape(a.shape)
@@ -280,9 +331,25 @@ def main(argv=None) -> int:
             p.add_argument("--colmajor-trace", dest="colmajor_trace", action="store_true",
                            help="address the trace in column-major instead of prepacked layout")
             p.add_argument("--max-events", dest="max_events", type=int, default=4 * 10 ** 9)
+    r = sub.add_parser("roofline")  # tilemul_main.cpp:482-488
+    r.add_argument("--peak", type=float, required=True, help="peak flops per second")
+    r.add_argument("--bw", type=float, required=True, help="memory bandwidth in bytes per second")
+    r.add_argument("--point", action="append", help="name=intensity_flops_per_byte (repeatable)")
+    r.add_argument("--format", default="csv", choices=["json", "human", "csv"])
+    r.add_argument("--out")
+    q = sub.add_parser("pareto")  # tilemul_main.cpp:492-501
+    q.add_argument("--cache", type=int, required=True, help="outer cache capacity in elements")
+    q.add_argument("--ratios", required=True, help="comma list of capacity ratios > 1")
+    q.add_argument("--shape", default="1024")
+    q.add_argument("--slack", type=float, default=1.0 / 16.0)
+    q.add_argument("--mr", type=int, default=4)
+    q.add_argument("--nr", type=int, default=12)
+    q.add_argument("--format", default="csv", choices=["json", "human", "csv"])
+    q.add_argument("--out")
     a = ap.parse_args(argv)
     try:
-        return {"run": cmd_run, "analyze": cmd_analyze, "simulate": cmd_simulate, "plan": cmd_plan}[a.cmd](a)
+        return {"run": cmd_run, "analyze": cmd_analyze, "simulate": cmd_simulate, "plan": cmd_plan,
+                "roofline": cmd_roofline, "pareto": cmd_pareto}[a.cmd](a)
     except (T.ValidationFailure, T.ParseError, T.InfeasibleError) as e:
         sys.stderr.write(f"{e}\n")
         return 1

@@ -459,6 +459,41 @@ def roofline_bound(intensity: float, peak: float, bandwidth: float) -> float:
     return _dbl(N.lib().tm_roofline_bound(intensity, peak, bandwidth))
 
 
+@dataclass
+class ParetoPoint:  # costmodel.hpp:286-293
+    ratio: float
+    inner_capacity: int
+    outer_block_k: int
+    outer_block_n: int
+    inner_block_m: int
+    inner_block_k: int
+    eff_outer_flops_per_element: float
+    eff_inner_flops_per_element: float
+
+
+def pareto_sweep(outer_capacity: int, ratios: Sequence[float], shape: Shape,
+                 opts: Optional["DeriveOptions"] = None) -> List[ParetoPoint]:  # costmodel.hpp:299-328
+    """Sweeps the capacity ratio of a cache pair: B2A1C0 (B in the outer
+    cache, A in the inner one, C in registers) with blocks derived under the
+    fit rules at each ratio, and both levels' modelled efficiencies."""
+    o = opts or DeriveOptions()
+    reg = max(o.micro.m_r * o.micro.n_r, 1)
+    d = parse_name("B2A1C0")
+    points = []
+    for r in sorted(ratios):
+        if not r > 1.0:
+            raise ValueError("ratios must be > 1")
+        inner = int(float(outer_capacity) / r)
+        if inner <= reg:
+            raise InfeasibleError(f"infeasible ratio {r}: the inner cache cannot hold even one register tile")
+        hier = CacheHierarchy([CacheLevel(0, reg), CacheLevel(1, inner), CacheLevel(2, outer_capacity)])
+        bs = derive_blocksizes(d, hier, shape, None, o)
+        rep = multilevel_cost(d, bs, hier, shape)
+        points.append(ParetoPoint(r, inner, bs.get(2, "k"), bs.get(2, "n"), bs.get(1, "m"), bs.get(1, "k"),
+                                  efficiency(rep, 2)[0], efficiency(rep, 1)[0]))
+    return points
+
+
 # --------------------------------------------------------------- the plan
 NUMERICS = {"dmma": 0, "fma": 1, "exact": 2}
 SCHEDULES = {"fused": 0, "faithful": 1}

@@ -175,11 +175,33 @@ def cachesim_cases():
     print("cachesim:", len(out["events"]), "event cases,", len(out["plans"]), "plans,", len(out["traces"]), "traces")
 
 
+def pareto_cases():
+    """Reference pareto_sweep outputs over seeded cache sizes, ratios and shapes."""
+    rng = np.random.default_rng(77)
+    out = []
+    for t in range(24):
+        outer = int(rng.choice([4096, 49152, 262144, 786432, 1 << 22]))
+        ratios = sorted(set(float(x) for x in rng.choice([1.5, 2, 4, 8, 16, 24, 64, 256], size=3)))
+        shape = tuple(int(x) for x in rng.integers(64, 8192, size=3))
+        slack = [1 / 16, 0.0, 0.25][t % 3]
+        mr, nr = [(4, 12), (8, 6), (2, 2)][t % 3]
+        case = {"outer": outer, "ratios": ratios, "shape": shape, "slack": slack, "mr": mr, "nr": nr}
+        try:
+            case["points"] = [list(p) for p in O.ref_pareto(outer, ratios, shape, slack, mr, nr)]
+        except ValueError as e:
+            case["error"] = str(e)
+        out.append(case)
+    json.dump(out, open(os.path.join(HERE, "pareto_cases.json"), "w"))
+    print("pareto:", len(out), "cases,", sum("error" in c for c in out), "rejected")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["host", "config1", "cachesim"]
+    which = sys.argv[1:] or ["host", "config1", "cachesim", "pareto"]
     if "host" in which:
         host_cases()
     if "config1" in which:
         config1()
     if "cachesim" in which:
         cachesim_cases()
+    if "pareto" in which:
+        pareto_cases()

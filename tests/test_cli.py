@@ -99,3 +99,24 @@ def test_simulate_json_csv_and_trace_dump(tmp_path):  # tilemul_main.cpp:179-229
 def test_simulate_refuses_long_traces(tmp_path):
     rc, _, err = cli(["simulate", "--hier", _desk_hier(tmp_path), "--max-events", "1000"] + DESK)
     assert rc == 2 and "--max-events" in err
+
+
+def test_roofline_regimes():  # acceptance.cpp:256-281 (criterion 7)
+    rc, out, _ = cli(["roofline", "--peak", "40e9", "--bw", "1e9", "--point", "A2C0=23.26", "--point", "B3A2C0=64.0"])
+    assert rc == 0
+    assert "A2C0,23.26," in out and ",bandwidth-bound" in out
+    assert "B3A2C0,64," in out and ",compute-bound" in out
+    rc, out, _ = cli(["roofline", "--peak", "40e9", "--bw", "1e9", "--point", "x=40", "--format", "json"])
+    j = json.loads(out)
+    assert rc == 0 and j["breakpoint_intensity"] == 40.0 and j["points"][0]["regime"] == "compute-bound"
+    rc, _, _ = cli(["roofline", "--peak", "1", "--bw", "1", "--point", "noequals"])
+    assert rc == 2
+
+
+def test_pareto_cli():  # tilemul_main.cpp:390-431
+    rc, out, _ = cli(["pareto", "--cache", "262144", "--ratios", "4,16", "--shape", "4096", "--format", "json"])
+    assert rc == 0
+    pts = json.loads(out)["points"]
+    assert [p["ratio"] for p in pts] == [4.0, 16.0] and pts[0]["inner_capacity"] == 65536
+    assert cli(["pareto", "--cache", "100", "--ratios", "64", "--shape", "64"])[0] == 1  # infeasible
+    assert cli(["pareto", "--cache", "100", "--ratios", "", "--shape", "64"])[0] == 2

@@ -15,6 +15,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+# L2-level block of the C2A1C0 plan (m x n); 1536 x 3072 = 72 SM-pair tiles, one wave
+L2M, L2N = (int(x) for x in os.environ.get("TC_L2_BLOCK", "1536x3072").split("x"))
+
+
 def main():
     import torch
 
@@ -28,7 +32,7 @@ def main():
     d = T.parse_name("C2A1C0")
     def plan(tile):
         bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(tile, 256)),
-                                 pinned=T.BlocksizeSet({(1, "m"): tile, (2, "m"): 1536, (2, "n"): 3072}))
+                                 pinned=T.BlocksizeSet({(1, "m"): tile, (2, "m"): L2M, (2, "n"): L2N}))
         return T.build_plan(d, bs, hier, T.Shape(m, n, k)), bs
 
     A64 = torch.empty(m * k, dtype=torch.float64, device="cuda")
@@ -38,7 +42,8 @@ def main():
     # live tcgen05 issue-rate peaks: bursts at full clocks, and ~200 ms launches under the power cap
     probe = {dt: T.measure_tc_peak(dt, 10) for dt in ("bf16", "tf32")}
     probe_sus = {dt: T.measure_tc_peak(dt, 3, sustained=True) for dt in ("bf16", "tf32")}
-    for dtype, tile in (("bf16", 256), ("bf16", 128), ("tf32", 256), ("tf32", 128)):
+    cases = os.environ.get("TC_CASES", "bf16:256,bf16:128,tf32:256,tf32:128").split(",")
+    for dtype, tile in ((c.split(":")[0], int(c.split(":")[1])) for c in cases):
         nest, bs = plan(tile)
         A = T.round_inputs(A64, dtype)
         B = T.round_inputs(B64, dtype)
