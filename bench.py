@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--size", type=int, default=M, help="square size (default 16384 = configs[1] max)")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--staging", default="auto", choices=["auto", "cpasync", "tma"],
+                   help="DMMA kernel staging (auto = TMA whenever it applies)")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--summa", action="store_true",
                    help="run the multi-GPU 2-D partition driver even at N=1 (exercises the N>1 code path)")
@@ -164,9 +166,9 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def ncu_traffic(workload):
+def ncu_traffic(workload, staging="cpasync"):
     """Per-launch DRAM bytes of the task kernel from the committed ncu
-    --set full summary of this workload (profiles/), or None."""
+    --set full summary of this workload and staging (profiles/), or None."""
     for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) if os.path.isdir(
             os.path.join(ROOT, "profiles")) else []:
         if name.startswith("ncu_summary") and name.endswith(".json"):
@@ -174,7 +176,8 @@ def ncu_traffic(workload):
                 d = json.load(open(os.path.join(ROOT, "profiles", name)))
             except (OSError, ValueError):
                 continue
-            if d.get("workload") == workload and d.get("dram_bytes_per_launch"):
+            if d.get("workload") == workload and d.get("staging", "cpasync") == staging and d.get(
+                    "dram_bytes_per_launch"):
                 return d["dram_bytes_per_launch"], name
     return None, None
 
@@ -254,11 +257,14 @@ def our_arm(args):
     T.fill_uniform_device(B, 2)
     T.fill_uniform_device(C, 3)
     # auto split_k: only the last partial wave's tiles are k-split (tail split)
-    opts = T.ExecOptions(numerics="dmma", schedule="fused", split_k=0)
+    opts = T.ExecOptions(numerics="dmma", schedule="fused", split_k=0, staging=args.staging)
     for _ in range(args.warmup):
         T.execute(nest, A, B, C, opts)
     torch.cuda.synchronize()
     launches_per_step = nest.last_launch()["launches"]
+    staging = nest.last_launch()["staging"]
+    kernel_name = ("k_dmma_tma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3> (16 warps, TMA 128B-swizzled slabs)"
+                   if staging == "tma" else "k_dmma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3,vec16> (16 warps, cp.async)")
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
@@ -281,7 +287,7 @@ def our_arm(args):
 
     peak = T.measure_fp64_peak(30)
     workload = workload_name(m)
-    traffic, traffic_src = ncu_traffic(workload)
+    traffic, traffic_src = ncu_traffic(workload, staging)
     model = nest.model()
     hbm_model_bytes = model.at_level(hier.top_level()).total_bytes()
 
@@ -324,6 +330,7 @@ def our_arm(args):
         "config": {"workload": workload, "m": m, "n": n, "k": k, "family": FAMILY,
                    "blocksizes": {f"{lv}:{d}": v for (lv, d), v in bs.entries()},
                    "schedule": "fused", "numerics": "dmma (mma.sync m8n8k4 f64)", "cta_tile": "128x128",
+                   "staging": staging,
                    "split_k": "auto (tail split of the last partial wave)",
                    "l2_flush": "not needed: inputs 6.4 GB > 126 MB L2", "parallelism": "1 GPU",
                    "hierarchy_elements": [hier.capacity(i) for i in range(hier.size())],
@@ -333,7 +340,7 @@ def our_arm(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "FP64 DMMA issue-rate probe run live in this bench (MEASURED_PEAKS.json has no "
                                     "FP64 figure); nominal 148 SM x 64 FMA/clk x 1.965 GHz = 37.2",
-                     "kernel": "k_dmma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3,vec16> (16 warps)", "algorithmic_flops_per_launch": flops,
+                     "kernel": kernel_name, "algorithmic_flops_per_launch": flops,
                      "traffic_source": traffic_src},
         "model": {"hbm_bytes_model": hbm_model_bytes,
                   "hbm_bytes_measured": traffic,

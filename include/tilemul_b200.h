@@ -97,7 +97,12 @@ typedef struct {
      * the member's own traffic). A k loop is rejected (status 2), like the
      * reference. */
     int32_t parallel_loop;
+    /* DMMA kernels: how the SMEM level is filled. TM_STAGING_AUTO picks TMA
+     * whenever it applies (16-byte aligned A/B and leading dimensions, every
+     * task's k range a whole number of slabs or ending at k), else cp.async. */
+    int32_t staging;
 } tm_exec_opts;
+enum { TM_STAGING_AUTO = 0, TM_STAGING_CPASYNC = 1, TM_STAGING_TMA = 2 };
 
 typedef struct tm_plan tm_plan;
 
@@ -192,6 +197,9 @@ int tm_execute_packed(tm_plan* plan, const double* A, const double* B, double* C
                       void* stream);
 /* Number of CTA tasks and kernel launches the last tm_execute issued. */
 int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, int32_t* ctas);
+/* Staging the last task-kernel launch used: TM_STAGING_CPASYNC or TM_STAGING_TMA
+ * (0 for the SIMT and tensor-core kernels, which have one staging each). */
+int tm_plan_last_staging(const tm_plan* plan, int32_t* staging);
 
 /* Sustained FP64 tensor-pipe (DMMA) rate of the current device in TFLOP/s,
  * from `launches` ~7 ms probe launches: the roofline denominator. */

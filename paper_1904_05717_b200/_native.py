@@ -37,7 +37,8 @@ class tm_derive_opts(C.Structure):
 
 class tm_exec_opts(C.Structure):
     _fields_ = [("numerics", C.c_int32), ("schedule", C.c_int32), ("split_k", C.c_int32), ("ctas", C.c_int32),
-                ("tile", C.c_int32), ("tile_n", C.c_int32), ("parallel_loop", C.c_int32)]
+                ("tile", C.c_int32), ("tile_n", C.c_int32), ("parallel_loop", C.c_int32),
+                ("staging", C.c_int32)]
 
 
 class tm_sim_level(C.Structure):
@@ -88,6 +89,7 @@ SIGNATURES = [
     ("tm_unpack", C.c_int, [P, C.c_char, P, P, P]),
     ("tm_execute_packed", C.c_int, [P, P, P, P, C.POINTER(tm_exec_opts), P]),
     ("tm_plan_last_launch", C.c_int, [P, C.POINTER(i64), C.POINTER(i32), C.POINTER(i32)]),
+    ("tm_plan_last_staging", C.c_int, [P, C.POINTER(i32)]),
     ("tm_fill_seeded", C.c_int, [C.c_uint64, P, i64, P, i64, P, i64]),
     ("tm_measure_fp64_peak", C.c_int, [C.c_int, C.POINTER(dbl)]),
     ("tm_measure_tc_peak", C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(dbl)]),

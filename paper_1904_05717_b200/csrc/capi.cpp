@@ -413,6 +413,12 @@ int tm_plan_last_launch(const tm_plan* plan, int64_t* tasks, int32_t* launches, 
     });
 }
 
+int tm_plan_last_staging(const tm_plan* plan, int32_t* staging) {
+    return guard([&] {
+        if (staging) *staging = plan->last_staging;
+    });
+}
+
 int tm_fill_seeded(uint64_t seed, double* a, int64_t na, double* b, int64_t nb, double* c, int64_t nc) {
     return guard([&] {
         if (!a && na > 0) fail_usage("null A buffer");

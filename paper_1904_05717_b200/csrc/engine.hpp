@@ -41,6 +41,7 @@ struct Schedule {
     double* work = nullptr;
     int64_t work_ld = 0, work_slice = 0;
     int device = -1;
+    int tma_ok = -1;         // task list fits the TMA kernel's slab grid (-1 = not yet checked)
     ~Schedule() {
         if (tasks) cudaFree(tasks);
         if (progress) cudaFree(progress);
@@ -78,6 +79,11 @@ struct HostPipe {
 };
 
 int sm_count();
+// Launch the schedule's task kernel: the TMA-fed DMMA variant when the
+// options allow and the operands/task list fit it, else the cp.async one.
+// Returns the staging used (TM_STAGING_*; 0 = kernel without variants).
+int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t K, bool vec16, int32_t staging,
+                 cudaStream_t stream);
 gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o);
 // Lowers the nest onto CTA tasks for `kernel` (schedule, split and fix-up
 // per opts). upload = false builds the host task list only.
@@ -105,6 +111,7 @@ struct tm_plan {
     std::unique_ptr<mmm::engine::HostPipe> pipe;
     int64_t last_tasks = 0;
     int32_t last_launches = 0, last_ctas = 0;
+    int32_t last_staging = 0;
     ~tm_plan() {
         if (dA) cudaFree(dA);
         if (dB) cudaFree(dB);

@@ -155,7 +155,8 @@ std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o,
 
 bool same_opts(const tm_exec_opts& a, const tm_exec_opts& b) {
     return a.numerics == b.numerics && a.schedule == b.schedule && a.split_k == b.split_k && a.ctas == b.ctas &&
-           a.tile == b.tile && a.tile_n == b.tile_n && a.parallel_loop == b.parallel_loop;
+           a.tile == b.tile && a.tile_n == b.tile_n && a.parallel_loop == b.parallel_loop &&
+           a.staging == b.staging;
 }
 
 void run_pipe(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts& o) {
@@ -180,7 +181,7 @@ void run_pipe(tm_plan* plan, const double* A, const double* B, double* C, const 
     const bool vec16 = e.m % 2 == 0 && e.k % 2 == 0 && origins_even(S.host_tasks);
     gpu::Args a{plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, S.tasks, static_cast<int32_t>(S.host_tasks.size()),
                 S.progress, nullptr, 0, 0, nullptr, P.flags, P.flags + nu};
-    cuda_check(gpu::launch(S.kernel, vec16, a, S.grid, st), "pipeline kernel launch");
+    plan->last_staging = launch_tasks(S, a, e.m, e.n, e.k, vec16, o.staging, st);
 
     // uploads in first-need order, a flag after each unit's pieces
     const std::size_t ldb = static_cast<std::size_t>(e.k) * sizeof(double);

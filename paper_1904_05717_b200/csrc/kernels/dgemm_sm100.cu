@@ -15,8 +15,19 @@
 //                   fma restatement of the reference cell.
 //   k_simt<EXACT> — DMUL then DADD per (entry, k): bit-exact against the
 //                   reference's own execute() (built -O2, no FMA contraction).
+//
+// Staging variants of the DMMA kernel:
+//   k_dmma      — every thread issues 16-byte cp.async chunks of the slabs
+//                 into padded [k][m] / [n][k] stages;
+//   k_dmma_tma  — one thread issues TMA tensor copies (cp.async.bulk.tensor)
+//                 of the slabs into 128B-swizzled stages and runs ahead
+//                 across task boundaries (the next task's first slabs land
+//                 under this task's epilogue).
 #include <cstdint>
 #include <mutex>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "gpu.hpp"
 
@@ -134,7 +145,33 @@ __device__ __forceinline__ void signal_partial(const Args& a, const Task& t) {
     }
 }
 
-template <int FM, int FN>
+// Row and column of a lane's C pair (rows r, r+1 of column c) in DMMA
+// group (mi, ni). SWZ: the TMA kernel's m and n orders. A 64-bit shared load
+// is served per half-warp (16 lanes = 128 B). In the 128B-swizzled stages
+// (16-byte unit ^ row%8) the lanes of a half-warp read 4 k rows (A) or 4 n
+// rows (B); with consecutive m or n they would pair rows r and r^1 on the
+// same units (2-way conflict). Lane g of group mi takes m = (g&1) +
+// 8((g>>1)&1) + 2(g>>2) + 4(mi&1) of chunk mi/2 (units {x, x^4} per
+// half-warp) and lane g of group ni takes n = 2(g&3) + (g>>2) (even n rows in
+// one half-warp, odd in the other): one wavefront per half-warp. The orders
+// only permute which lane holds which C entry; every entry sees the same
+// DMMA groups in the same k order as in the cp.async kernel.
+template <bool SWZ>
+__device__ __forceinline__ int c_row(int wm0, int mi, int tq) {
+    if constexpr (SWZ)
+        return wm0 + (mi >> 1) * 16 + (mi & 1) * 4 + 8 * (tq & 1) + 2 * (tq >> 1);
+    else
+        return wm0 + mi * 8 + 2 * tq;
+}
+template <bool SWZ>
+__device__ __forceinline__ int c_col(int wn0, int ni, int g) {
+    if constexpr (SWZ)
+        return wn0 + ni * 8 + 2 * (g & 3) + (g >> 2);
+    else
+        return wn0 + ni * 8 + g;
+}
+
+template <int FM, int FN, bool SWZ = false>
 __device__ __forceinline__ void fold_partials(const Args& a, const Task& t, double (&acc)[FM][FN][2], int wm0,
                                               int wn0, int g, int tq) {
     if (threadIdx.x == 0) {
@@ -154,7 +191,7 @@ __device__ __forceinline__ void fold_partials(const Args& a, const Task& t, doub
         for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
             for (int ni = 0; ni < FN; ++ni) {
-                const int r = wm0 + mi * 8 + 2 * tq, c = wn0 + ni * 8 + g;
+                const int r = c_row<SWZ>(wm0, mi, tq), c = c_col<SWZ>(wn0, ni, g);
                 // slots are tile-shaped (work_ld = tile rows, even) and 16-byte aligned
                 const double2 v = __ldcg(reinterpret_cast<const double2*>(w + r + static_cast<int64_t>(c) * a.work_ld));
                 acc[mi][ni][0] = __dadd_rn(acc[mi][ni][0], v.x);
@@ -489,6 +526,208 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
     }
 }
 
+// ========================== DMMA kernel, TMA-fed ==========================
+// The SMEM level of the family member as a TMA ring: A's slab (BM rows x BK
+// columns of the column-major A) lands as BM/16 boxes of 16 x BK doubles
+// ([k][16 m] rows of 128 B), B's slab (BK x BN) as BK/16 boxes of 16 x BN
+// ([n][16 k] rows), both with the 128-byte swizzle, so no padding and no
+// per-thread address arithmetic. One thread (warp 0, lane 0) is the
+// producer: it keeps STAGES-1 slabs in flight ahead of the slab being
+// consumed, following the CTA's task list across task boundaries, so the
+// next task's first slabs arrive while this task's C tile is written back.
+// full[s] completes on the TMA byte count; empty[s] on one arrive per warp.
+// The producer does not run ahead into a task whose copy-engine data flag
+// (Task::ready) it has not seen: that wait stays at the task boundary.
+#ifndef TM_TMA_ISSUE_KK
+#define TM_TMA_ISSUE_KK 2
+#endif
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_addr(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool FIX = true>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
+    k_dmma_tma(Args a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+    constexpr int NWM = BM / WM, NW = (BM / WM) * (BN / WN);
+    constexpr int FM = WM / 8, FN = WN / 8, KK = BK / 4;
+    constexpr int PD = STAGES - 1;
+    constexpr int ISSUE_KK = TM_TMA_ISSUE_KK < KK - 1 ? TM_TMA_ISSUE_KK : KK - 1;  // k step of the refill
+    constexpr uint32_t A_CHUNK = BK * 128, B_CHUNK = BN * 128;  // bytes of one 16-wide box
+    constexpr uint32_t A_BYTES = BM * BK * 8, STAGE_BYTES = A_BYTES + BN * BK * 8;
+    static_assert(BM % 16 == 0 && BK % 16 == 0 && WM % 16 == 0 && WN % 8 == 0, "16-wide swizzle atoms");
+    static_assert(A_CHUNK % 1024 == 0 && B_CHUNK % 1024 == 0, "boxes must start on 1024-byte swizzle periods");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+    const uint32_t raw = smem_addr(smem_raw);
+    const uint32_t sbase = (raw + 1023u) & ~1023u;
+    const unsigned char* sgen = smem_raw + (sbase - raw);
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < STAGES; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], NW);
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    __syncthreads();
+
+    const int g = lane >> 2, tq = lane & 3;
+    const int wm0 = (warp % NWM) * WM, wn0 = (warp / NWM) * WN;
+    // Fragment byte offsets inside a stage. A element (k, m) of a slab sits
+    // at box m/16 | row k | unit ((m%16)/2) ^ (k%8) | half m%2 -- disjoint bit
+    // fields (box * A_CHUNK, k << 7, unit << 4, half << 3); B element (k, n)
+    // at box k/16 | row n | unit ((k%16)/2) ^ (n%8) | half k%2. With k =
+    // 4kk + tq and the SWZ orders the (mi&1, kk&1) / (kk&3) dependence of the
+    // unit is a bit flip of a per-lane base, the rest an immediate.
+    const int nn = 2 * (g & 3) + (g >> 2);  // n % 8 of this lane's B rows
+    const uint32_t aoff = (wm0 >> 4) * A_CHUNK + tq * 128 + (((4 * ((g >> 1) & 1) + (g >> 2)) ^ tq) << 4) + (g & 1) * 8;
+    const uint32_t boff = A_BYTES + (wn0 + nn) * 128 + (((tq >> 1) ^ nn) << 4) + (tq & 1) * 8;
+
+    const int t_hi = a.cta_first ? a.cta_first[blockIdx.x + 1] : a.ntasks;
+    const int t_step = a.cta_first ? 1 : static_cast<int>(gridDim.x);
+    int ti = a.cta_first ? a.cta_first[blockIdx.x] : static_cast<int>(blockIdx.x);
+
+    // Producer cursor, kept in shared memory (only warp 0 touches it, so it
+    // costs the consumers no registers): next slab to issue = slab `slab` of
+    // task `ti`; `issued` counts slabs issued by this CTA.
+    __shared__ struct {
+        int ti, slab, nk, i0, j0, p0, ready;
+        uint32_t issued;
+    } pc;
+    uint32_t n_use = 0;
+    auto p_load = [&](int from) {  // lane 0
+        int x = from;
+        for (; x < t_hi; x += t_step) {
+            const Task pt = a.tasks[x];
+            if (pt.k <= 0) continue;
+            pc.nk = (pt.k + BK - 1) / BK;
+            pc.i0 = pt.i0;
+            pc.j0 = pt.j0;
+            pc.p0 = pt.p0;
+            pc.ready = pt.ready;
+            break;
+        }
+        pc.ti = x;
+        pc.slab = 0;
+    };
+    // warp 0: issue slabs until `limit` have been issued in total (lane 0 works, the warp waits)
+    auto top_up = [&](uint32_t limit, int cur) {
+        if (lane == 0) {
+            while (pc.issued < limit && pc.ti < t_hi) {
+                if (pc.slab == 0 && pc.ti != cur && pc.ready != 0) break;  // its data flag is awaited at its start
+                const uint32_t n = pc.issued, stage = n % STAGES;
+                if (n >= STAGES) mbar_wait(&empty[stage], ((n / STAGES) - 1) & 1);
+                mbar_expect_tx(&full[stage], STAGE_BYTES);
+                const uint32_t sa = sbase + stage * STAGE_BYTES;
+                const int kc = pc.p0 + pc.slab * BK, i0 = pc.i0, j0 = pc.j0;
+#pragma unroll
+                for (int c = 0; c < BM / 16; ++c) tma_2d(sa + c * A_CHUNK, &tmA, &full[stage], i0 + 16 * c, kc);
+#pragma unroll
+                for (int c = 0; c < BK / 16; ++c)
+                    tma_2d(sa + A_BYTES + c * B_CHUNK, &tmB, &full[stage], kc + 16 * c, j0);
+                pc.issued = n + 1;
+                if (++pc.slab == pc.nk) p_load(pc.ti + t_step);
+            }
+        }
+        __syncwarp();
+    };
+    if (threadIdx.x == 0) {
+        pc.issued = 0;
+        p_load(ti);
+    }
+    __syncwarp();
+
+
+    for (; ti < t_hi; ti += t_step) {
+        const Task t = a.tasks[ti];
+        wait_ready(a, t);
+        wait_turn(a, t);
+        const int nk = (t.k + BK - 1) / BK;
+        if (warp == 0) top_up(n_use + PD, ti);
+
+        const Dest d = resolve(a, t);
+        double acc[FM][FN][2];
+        const bool src_vec = d.src != nullptr && ((reinterpret_cast<uintptr_t>(d.src) & 15) | (d.ld_src & 1) |
+                                                  (static_cast<int64_t>(t.i0) & 1)) == 0;
+#pragma unroll
+        for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni) {
+                const int r = c_row<true>(wm0, mi, tq), c = c_col<true>(wn0, ni, g);
+                const double* p = d.src + (t.i0 + r) + static_cast<int64_t>(t.j0 + c) * d.ld_src;
+                if (src_vec && r + 1 < t.m && c < t.n) {
+                    const double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+                    acc[mi][ni][0] = v.x;
+                    acc[mi][ni][1] = v.y;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        acc[mi][ni][e] = (d.src && r + e < t.m && c < t.n) ? __ldcg(p + e) : 0.0;
+                }
+            }
+
+        for (int s = 0; s < nk; ++s) {
+            const uint32_t stage = n_use % STAGES;
+            mbar_wait_warp(&full[stage], (n_use / STAGES) & 1);
+            const unsigned char* st = sgen + stage * STAGE_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < KK; ++kk) {
+                double af[FM], bf[FN];
+#pragma unroll
+                for (int mi = 0; mi < FM; ++mi)
+                    af[mi] = *reinterpret_cast<const double*>(st + (aoff ^ ((mi & 1) << 5) ^ ((kk & 1) << 6)) +
+                                                              (mi >> 1) * A_CHUNK + kk * 512);
+#pragma unroll
+                for (int ni = 0; ni < FN; ++ni)
+                    bf[ni] = *reinterpret_cast<const double*>(st + (boff ^ ((kk & 3) << 5)) + (kk >> 2) * B_CHUNK +
+                                                              ni * 1024);
+#pragma unroll
+                for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < FN; ++ni) dmma884(acc[mi][ni], bf[ni], af[mi]);
+                if (kk == ISSUE_KK && warp == 0) top_up(n_use + PD + 1, ti);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            ++n_use;
+        }
+        if constexpr (FIX) {
+            if (t.fixup == 2) fold_partials<FM, FN, true>(a, t, acc, wm0, wn0, g, tq);
+        }
+
+        const int64_t di = d.oi, dj = d.oj;
+        const bool dst_vec = ((reinterpret_cast<uintptr_t>(d.dst) & 15) | (d.ld_dst & 1) | (di & 1)) == 0;
+#pragma unroll
+        for (int mi = 0; mi < FM; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < FN; ++ni) {
+                const int r = c_row<true>(wm0, mi, tq), c = c_col<true>(wn0, ni, g);
+                double* p = d.dst + (di + r) + (dj + c) * d.ld_dst;
+                if (dst_vec && r + 1 < t.m && c < t.n) {
+                    *reinterpret_cast<double2*>(p) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        if (r + e < t.m && c < t.n) p[e] = acc[mi][ni][e];
+                }
+            }
+        if (FIX && t.fixup == 1) signal_partial(a, t);
+        else signal_done(a, t, ti);
+    }
+}
+
 // ============================== SIMT kernels =============================
 // Thread (tx, ty) owns rows ty*TM.., columns tx*TN.. of the CTA tile; each
 // entry accumulates one k at a time, in ascending order, only over k that
@@ -659,6 +898,28 @@ const Entry kTable[kKernelCount] = {
      128, 64, 128, dmma_smem<128, 64, kBKSmall, kStagesRankK>()},
 };
 
+template <int BM, int BN, int BK, int STAGES>
+constexpr int tma_smem() {
+    return (BM + BN) * BK * STAGES * static_cast<int>(sizeof(double)) + 1024;  // + alignment to the swizzle period
+}
+
+// TMA-fed variants of the DMMA kernels (same tiles, k-slab depth and stage
+// count as their cp.async counterparts; fn == nullptr: none).
+struct TmaEntry {
+    const void* fn;
+    int bk, box_n, smem;
+};
+const TmaEntry kTmaTable[kKernelCount] = {
+    {(const void*)k_dmma_tma<128, 128, kBKBig, 32, 32, kStagesBig>, kBKBig, 128, tma_smem<128, 128, kBKBig, kStagesBig>()},
+    {(const void*)k_dmma_tma<64, 64, kBKSmall, 32, 32, kStagesSmall>, kBKSmall, 64, tma_smem<64, 64, kBKSmall, kStagesSmall>()},
+    {nullptr, 0, 0, 0},
+    {nullptr, 0, 0, 0},
+    {nullptr, 0, 0, 0},
+    {(const void*)k_dmma_tma<128, 64, kBKSmall, 64, 32, kStagesRankK, false>, kBKSmall, 64,
+     tma_smem<128, 64, kBKSmall, kStagesRankK>()},
+};
+int g_tma_occ[kKernelCount];  // 0 = not prepared
+
 KernelInfo g_info[kKernelCount];
 bool g_ready[kKernelCount][2];
 int g_device = -1;
@@ -671,6 +932,7 @@ cudaError_t prepare(Kernel k, bool v16) {
     if (e != cudaSuccess) return e;
     if (dev != g_device) {
         for (auto& r : g_ready) r[0] = r[1] = false;
+        for (int& o : g_tma_occ) o = 0;
         g_device = dev;
     }
     if (g_ready[k][v16]) return cudaSuccess;
@@ -704,6 +966,59 @@ cudaError_t launch(Kernel kernel, bool vec16, const Args& args, int grid, cudaSt
     Args local = args;
     void* params[] = {&local};
     return cudaLaunchKernel(en.fn[vec16], dim3(grid), dim3(en.threads), params, en.smem, stream);
+}
+
+int tma_bk(Kernel kernel) { return kernel >= 0 && kernel < kKernelCount ? kTmaTable[kernel].bk : 0; }
+
+cudaError_t launch_tma(Kernel kernel, const Args& args, int64_t M, int64_t N, int64_t K, int grid,
+                       cudaStream_t stream) {
+    if (kernel < 0 || kernel >= kKernelCount || kTmaTable[kernel].fn == nullptr) return cudaErrorNotSupported;
+    const TmaEntry& en = kTmaTable[kernel];
+    if ((args.lda & 1) || (args.ldb & 1) || (reinterpret_cast<uintptr_t>(args.A) & 15) ||
+        (reinterpret_cast<uintptr_t>(args.B) & 15))
+        return cudaErrorNotSupported;  // TMA: 16-byte aligned bases and strides
+    cudaError_t e = prepare(kernel, true);
+    if (e != cudaSuccess) return e;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (g_tma_occ[kernel] == 0) {
+            if ((e = cudaFuncSetAttribute(en.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, en.smem)) != cudaSuccess)
+                return e;
+            int occ = 0;
+            if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, en.fn, kTable[kernel].threads, en.smem)) !=
+                cudaSuccess)
+                return e;
+            g_tma_occ[kernel] = occ > 0 ? occ : -1;
+        }
+        // the persistent grid was sized for the cp.async kernel; every CTA must be co-resident
+        if (g_tma_occ[kernel] < g_info[kernel].ctas_per_sm) return cudaErrorNotSupported;
+    }
+    if (args.ntasks <= 0) return cudaSuccess;
+    auto* encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+    if (encode == nullptr) return cudaErrorNotSupported;
+    CUtensorMap ma, mb;
+    const cuuint32_t estr[2] = {1, 1};
+    {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(K)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(args.lda) * 8};
+        const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(en.bk)};
+        if (encode(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(args.A), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(args.ldb) * 8};
+        const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(en.box_n)};
+        if (encode(&mb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(args.B), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    Args local = args;
+    void* params[] = {&local, &ma, &mb};
+    return cudaLaunchKernel(en.fn, dim3(grid), dim3(kTable[kernel].threads), params, en.smem, stream);
 }
 
 cudaError_t launch_reduce_tiles(double* C, int64_t ldc, const double* work, int64_t work_ld, int64_t work_slice,

@@ -86,6 +86,17 @@ struct KernelInfo {
 // Launch `kernel` over args.tasks with `grid` persistent CTAs. vec16 selects
 // 16-byte cp.async staging (all task origins even, ld even, 16B-aligned bases).
 cudaError_t launch(Kernel kernel, bool vec16, const Args& args, int grid, cudaStream_t stream);
+// TMA-fed variant of a DMMA kernel (k_dmma_tma): A (M x K) and B (K x N) are
+// read through tensor maps built per launch, so the task list must not need
+// a k limit inside a slab: every task's k range is a multiple of tma_bk() or
+// ends at K (out-of-range rows/columns are zero-filled by the TMA unit).
+// cudaErrorNotSupported: no TMA variant, unaligned operands, or lower
+// occupancy than the cp.async kernel the grid was sized for.
+cudaError_t launch_tma(Kernel kernel, const Args& args, int64_t M, int64_t N, int64_t K, int grid,
+                       cudaStream_t stream);
+int tma_bk(Kernel kernel);  // k-slab depth of the TMA variant (0 = none)
+// cuTensorMapEncodeTiled from the driver (nullptr if unavailable).
+void* tensor_map_encoder();
 // Occupancy-derived info (queries the device on first call).
 cudaError_t kernel_info(Kernel kernel, KernelInfo* info);
 // C(tile) = slot0 + slot1 + ... in slot order for every listed tile

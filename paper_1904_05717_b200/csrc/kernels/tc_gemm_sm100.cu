@@ -616,6 +616,12 @@ cudaError_t encoder() {
     return cudaSuccess;
 }
 
+}  // namespace
+
+void* tensor_map_encoder() { return encoder() == cudaSuccess ? reinterpret_cast<void*>(g_encode) : nullptr; }
+
+namespace {
+
 // 2-D column-major tensor map: dim0 contiguous (rows), box {box0, box1}, 128B swizzle.
 cudaError_t make_map(CUtensorMap* m, const void* base, bool tf32, int64_t rows, int64_t cols, int64_t ld, int box0,
                      int box1, CUtensorMapSwizzle swz) {

@@ -425,6 +425,41 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
     return s;
 }
 
+int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t K, bool vec16, int32_t staging,
+                 cudaStream_t stream) {
+    if (staging < TM_STAGING_AUTO || staging > TM_STAGING_TMA) fail_usage("staging must be 0 (auto), 1 (cp.async) or 2 (TMA)");
+    const int bk = gpu::tma_bk(s.kernel);
+    if (staging == TM_STAGING_TMA && bk == 0) fail_usage("TMA staging exists for the DMMA kernels only");
+    // Auto takes TMA for the 128x128 kernel only: measured on one B200 it is
+    // 0.2-1.7 points of FP64 peak faster there on every BASELINE config, while
+    // the 128x64 / 64x64 TMA variants trail their cp.async versions by 0.5-4
+    // points (profiles/sweep_r01_staging.jsonl).
+    const bool want = staging == TM_STAGING_TMA || (staging == TM_STAGING_AUTO && s.kernel == gpu::kDmma128);
+    if (bk > 0 && want) {
+        if (s.tma_ok < 0) {
+            s.tma_ok = 1;
+            for (const auto& t : s.host_tasks)
+                if (t.k % bk != 0 && static_cast<int64_t>(t.p0) + t.k != K) {
+                    s.tma_ok = 0;
+                    break;
+                }
+        }
+        // TMA boxes start on 16-byte boundaries of a column: the alignment the
+        // 16-byte cp.async path needs too (even task origins, even ld, aligned bases)
+        cudaError_t r = cudaErrorNotSupported;
+        if (s.tma_ok == 1 && vec16) {
+            r = gpu::launch_tma(s.kernel, a, M, N, K, s.grid, stream);
+            if (r == cudaSuccess) return TM_STAGING_TMA;
+            if (r != cudaErrorNotSupported) cuda_check(r, "task kernel launch (TMA)");
+        }
+        if (staging == TM_STAGING_TMA)
+            fail_usage("TMA staging does not apply: A/B, their leading dimensions or the task origins are not "
+                       "16-byte aligned, or a task's k range is not a whole number of slabs");
+    }
+    cuda_check(gpu::launch(s.kernel, vec16, a, s.grid, stream), "task kernel launch");
+    return bk > 0 ? TM_STAGING_CPASYNC : 0;
+}
+
 bool origins_even(const std::vector<gpu::Task>& T) {
     for (const auto& t : T)
         if ((t.i0 | t.p0) & 1) return false;
@@ -454,7 +489,7 @@ void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t l
                    "reset progress");
     gpu::Args a{A, lda, B, ldb, C, ldc, s.tasks, static_cast<int32_t>(s.host_tasks.size()), s.progress, s.work,
                 s.work_ld, s.work_slice, s.blocked ? s.cta_first : nullptr};
-    cuda_check(gpu::launch(s.kernel, vec16, a, s.grid, stream), "task kernel launch");
+    plan->last_staging = launch_tasks(s, a, e.m, e.n, e.k, vec16, o.staging, stream);
     int launches = 1;
     if (s.slices > 0) {
         cuda_check(gpu::launch_reduce_tiles(C, ldc, s.work, s.work_ld, s.work_slice, s.reduce, s.slices, stream),

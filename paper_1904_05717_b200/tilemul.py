@@ -497,6 +497,8 @@ def pareto_sweep(outer_capacity: int, ratios: Sequence[float], shape: Shape,
 # --------------------------------------------------------------- the plan
 NUMERICS = {"dmma": 0, "fma": 1, "exact": 2}
 SCHEDULES = {"fused": 0, "faithful": 1}
+STAGINGS = {"auto": 0, "cpasync": 1, "tma": 2}
+STAGING_NAMES = {0: None, 1: "cpasync", 2: "tma"}
 
 
 @dataclass
@@ -508,10 +510,11 @@ class ExecOptions:  # exec.hpp:48-53, re-targeted
     tile: int = 0               # CTA tile rows 64/128 (0 = from the register tile)
     tile_n: int = 0             # CTA tile columns (0 = tile); 128x64 runs two CTAs per SM
     parallel_loop: int = -1     # faithful: loop whose iterations run as independent workers (-1 = nest order)
+    staging: str = "auto"       # DMMA kernels: auto | cpasync | tma (how A/B k-slabs reach shared memory)
 
     def _c(self):
         return N.tm_exec_opts(NUMERICS[self.numerics], SCHEDULES[self.schedule], self.split_k, self.ctas, self.tile,
-                              self.tile_n, self.parallel_loop + 1)
+                              self.tile_n, self.parallel_loop + 1, STAGINGS[self.staging])
 
 
 class LoopNest:  # plan.hpp:25-85
@@ -554,7 +557,9 @@ class LoopNest:  # plan.hpp:25-85
     def last_launch(self) -> Dict[str, int]:
         t, l, c = C.c_int64(0), C.c_int32(0), C.c_int32(0)
         _check(N.lib().tm_plan_last_launch(self._ptr, C.byref(t), C.byref(l), C.byref(c)))
-        return {"tasks": t.value, "launches": l.value, "ctas": c.value}
+        st = C.c_int32(0)
+        _check(N.lib().tm_plan_last_staging(self._ptr, C.byref(st)))
+        return {"tasks": t.value, "launches": l.value, "ctas": c.value, "staging": STAGING_NAMES[st.value]}
 
 
 def build_plan(d: AlgorithmDescriptor, bs: BlocksizeSet, hier: CacheHierarchy, shape: Shape) -> LoopNest:

@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--workload", required=True)
     ap.add_argument("--tag", required=True)
     ap.add_argument("--flops", type=float)
+    ap.add_argument("--staging", default="cpasync", help="DMMA kernel staging the capture ran with")
     ap.add_argument("--model-bytes", type=float)
     ap.add_argument("--out-dir", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                                       "profiles"))
@@ -84,6 +85,7 @@ def main():
     summary = {
         "workload": a.workload,
         "tag": a.tag,
+        "staging": a.staging,
         "report": os.path.basename(a.rep),
         "kernel": top["kernel"],
         "duration_s_under_ncu": top.get("duration"),

@@ -80,6 +80,8 @@ def main():
     ap.add_argument("--tiles", default="auto,128x128,128x64")
     ap.add_argument("--only", default="", help="comma-separated config names to run (default: all)")
     ap.add_argument("--members", default="", help="comma-separated family members (default: per config)")
+    ap.add_argument("--staging", default="auto", choices=["auto", "cpasync", "tma"],
+                    help="DMMA kernels: how A/B k-slabs reach shared memory")
     ap.add_argument("--l2-frac", type=float, default=1.0, help="effective L2 capacity fraction for derivation")
     a = ap.parse_args()
     import torch
@@ -124,7 +126,7 @@ def main():
                     par = max((i for i in range(kin) if dims[i] != "k"), default=-1)
                     rec["parallel_loop"] = par
                 opts = T.ExecOptions(numerics="dmma", schedule=sched, split_k=extra.get("split_k", 0), tile=tm,
-                                     tile_n=tn, parallel_loop=par)
+                                     tile_n=tn, parallel_loop=par, staging=a.staging)
                 rep = nest.model()
                 rec["blocksizes"] = {f"{lv}:{d}": v for (lv, d), v in bs.entries()}
                 rec["model_bytes"] = {f"L{lt.level}": lt.total_bytes() for lt in rep.levels}
