@@ -42,6 +42,7 @@ struct Schedule {
     int64_t work_ld = 0, work_slice = 0;
     int device = -1;
     int tma_ok = -1;         // task list fits the TMA kernel's slab grid (-1 = not yet checked)
+    int64_t max_task_k = 0;  // longest task k range (set with tma_ok)
     ~Schedule() {
         if (tasks) cudaFree(tasks);
         if (progress) cudaFree(progress);

@@ -430,20 +430,28 @@ int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t 
     if (staging < TM_STAGING_AUTO || staging > TM_STAGING_TMA) fail_usage("staging must be 0 (auto), 1 (cp.async) or 2 (TMA)");
     const int bk = gpu::tma_bk(s.kernel);
     if (staging == TM_STAGING_TMA && bk == 0) fail_usage("TMA staging exists for the DMMA kernels only");
-    // Auto takes TMA for the 128x128 kernel only: measured on one B200 it is
-    // 0.2-1.7 points of FP64 peak faster there on every BASELINE config, while
-    // the 128x64 / 64x64 TMA variants trail their cp.async versions by 0.5-4
-    // points (profiles/sweep_r01_staging.jsonl).
-    const bool want = staging == TM_STAGING_TMA || (staging == TM_STAGING_AUTO && s.kernel == gpu::kDmma128);
-    if (bk > 0 && want) {
-        if (s.tma_ok < 0) {
-            s.tma_ok = 1;
-            for (const auto& t : s.host_tasks)
-                if (t.k % bk != 0 && static_cast<int64_t>(t.p0) + t.k != K) {
-                    s.tma_ok = 0;
-                    break;
-                }
+    if (bk > 0 && s.tma_ok < 0) {
+        s.tma_ok = 1;
+        s.max_task_k = 0;
+        for (const auto& t : s.host_tasks) {
+            if (t.k % bk != 0 && static_cast<int64_t>(t.p0) + t.k != K) s.tma_ok = 0;
+            s.max_task_k = std::max<int64_t>(s.max_task_k, t.k);
         }
+    }
+    // Auto takes TMA for the 128x128 kernel when no task is longer than
+    // kTmaAutoMaxK. Measured on one B200: TMA is 0.4-1.7
+    // points of FP64 peak faster than cp.async on every config, but its CTAs
+    // drift apart along long k ranges (the copies never stall them), so the
+    // wave stops sharing A/B panels in L2: HBM reads at 16384^3 grow 4-6x
+    // (1.6x / 2.2x at k = 4096 / 8192 with 16384^2 C, equal at 4096^3). A
+    // wave gate (CTAs of a round wait for the round's average k progress)
+    // restored the traffic but cost 2-4 points, more than TMA gains
+    // (profiles/tma_l2_r01.json). The 128x64 / 64x64 TMA variants trail
+    // cp.async by 0.5-4 points.
+    constexpr int64_t kTmaAutoMaxK = 4096;
+    const bool want = staging == TM_STAGING_TMA ||
+                      (staging == TM_STAGING_AUTO && s.kernel == gpu::kDmma128 && s.max_task_k <= kTmaAutoMaxK);
+    if (bk > 0 && want) {
         // TMA boxes start on 16-byte boundaries of a column: the alignment the
         // 16-byte cp.async path needs too (even task origins, even ld, aligned bases)
         cudaError_t r = cudaErrorNotSupported;

@@ -190,8 +190,7 @@ def test_tma_host_pipeline_bitwise():
         T.execute(nest, a, b, hc, T.ExecOptions(staging=staging))
         assert nest.last_launch()["staging"] == staging
         outs[staging] = hc
-    dev_out, st = run(nest, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), c)
-    assert st == "tma"
+    dev_out, _ = run(nest, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), c)
     assert np.array_equal(outs["tma"].view(np.uint64), outs["cpasync"].view(np.uint64))
     assert np.array_equal(outs["tma"].view(np.uint64), dev_out.view(np.uint64))
 
@@ -217,3 +216,24 @@ def test_tma_config1_golden_entries():
     assert abs(got[0] - g["C0"]) <= 4 * k * H.U64 * ab0
     ref, _ = run(nest, A, B, np.zeros(m * n), split_k=0, staging="cpasync")
     assert np.array_equal(got, ref)
+
+
+def test_tma_long_k_auto_stays_cpasync():
+    """Tasks longer than 4096 in k: auto stays on cp.async (TMA CTAs drift
+    apart along long k and lose the wave's L2 sharing, profiles/tma_l2_r01.json);
+    an explicit TMA launch is bitwise equal."""
+    m = n = 512
+    k = 8192 + 64
+    nest = fused_nest(m, n, k)
+    a, b, c = O.fill_uniform(77, [(m, k), (k, n), (m, n)])
+    A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    ref, st = run(nest, A, B, c, split_k=1)
+    assert st == "cpasync"
+    got, st = run(nest, A, B, c, split_k=1, staging="tma")
+    assert st == "tma"
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    ii = np.arange(0, m, 7)
+    jj = (ii * 3) % n
+    want, ab = O.entries(k, a, m, b, k, c, m, ii, jj)
+    ok, worst = H.entrywise_ok(got[ii + jj * m], want, ab, k, c0=c[ii + jj * m])
+    assert ok, worst

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--staging", default="auto")
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--ld-pad", type=int, default=0, help="leading-dimension padding (elements) of A, B and C")
     a = ap.parse_args()
     import torch
     from paper_1904_05717_b200 import planner, tilemul as T
@@ -30,11 +31,15 @@ def main():
     hier = planner.gpu_hierarchy_effective(128)
     bs = planner.derive_for_gpu(a.family, (m, n, k), hier)
     nest = T.build_plan(T.parse_name(a.family), bs, hier, T.Shape(m, n, k))
-    A = torch.empty(m * k, dtype=torch.float64, device="cuda")
-    B = torch.empty(k * n, dtype=torch.float64, device="cuda")
-    C = torch.empty(m * n, dtype=torch.float64, device="cuda")
-    for x, s in ((A, 1), (B, 2), (C, 3)):
+    P = a.ld_pad
+    Ab = torch.empty(k * (m + P), dtype=torch.float64, device="cuda")
+    Bb = torch.empty(n * (k + P), dtype=torch.float64, device="cuda")
+    Cb = torch.empty(n * (m + P), dtype=torch.float64, device="cuda")
+    for x, s in ((Ab, 1), (Bb, 2), (Cb, 3)):
         T.fill_uniform_device(x, s)
+    A = Ab.view(k, m + P).t()[:m, :]
+    B = Bb.view(n, k + P).t()[:k, :]
+    C = Cb.view(n, m + P).t()[:m, :]
     opts = T.ExecOptions(numerics="dmma", split_k=a.split, tile=a.tile, tile_n=a.tile_n, staging=a.staging)
     for _ in range(1 + a.reps):
         T.execute(nest, A, B, C, opts)
