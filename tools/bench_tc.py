@@ -79,6 +79,35 @@ def main():
                           "blocksizes": {f"{lv}:{dd}": v for (lv, dd), v in bs.entries()},
                           "launch": nest.last_launch(), "clocks": clk.summary()}), flush=True)
         del A, B, C
+    # cuBLAS at the same shape in the same process and power state (library
+    # reference, not our path): bf16 in/out (torch.matmul), tf32 in / fp32 out
+    if os.environ.get("TC_CUBLAS", "1") == "1":
+        import bench
+
+        for dtype in ("bf16", "tf32"):
+            torch.backends.cuda.matmul.allow_tf32 = dtype == "tf32"
+            dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+            X = A64.view(k, m).t().to(dt)
+            Y = B64.view(n, k).t().to(dt)
+            for _ in range(2):
+                Z = X @ Y
+            torch.cuda.synchronize()
+            ts = []
+            clk = bench.ClockSampler(0)
+            clk.__enter__()
+            for _ in range(40):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                Z = X @ Y
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e-3)
+            clk.__exit__(None, None, None)
+            t = statistics.median(ts)
+            print(json.dumps({"config": "config4", "impl": "cuBLAS (torch.matmul) reference", "dtype": dtype,
+                              "shape": [m, n, k], "seconds": t, "tflops": 2.0 * m * n * k / t / 1e12,
+                              "output": "bf16" if dtype == "bf16" else "fp32", "clocks": clk.summary()}), flush=True)
+            del X, Y, Z
 
 
 if __name__ == "__main__":
