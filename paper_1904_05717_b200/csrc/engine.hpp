@@ -85,7 +85,9 @@ int sm_count();
 // Returns the staging used (TM_STAGING_*; 0 = kernel without variants).
 int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t K, bool vec16, int32_t staging,
                  cudaStream_t stream);
-gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o);
+// `tma`: the operands allow TMA staging (16-byte aligned bases and leading
+// dimensions, staging not forced to cp.async).
+gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o, bool tma);
 // Lowers the nest onto CTA tasks for `kernel` (schedule, split and fix-up
 // per opts). upload = false builds the host task list only.
 std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, cudaStream_t stream,

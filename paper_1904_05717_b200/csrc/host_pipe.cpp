@@ -111,7 +111,7 @@ std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o,
     Nest first = plan.nest;
     first.ext.n = P->ncut[1];
     first.ext.k = P->kcut[1];
-    const gpu::Kernel kernel = pick_kernel(first, uo);
+    const gpu::Kernel kernel = pick_kernel(first, uo, uo.staging != TM_STAGING_CPASYNC && e.m % 2 == 0 && e.k % 2 == 0);
     gpu::KernelInfo info{};
     cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
     const i64 mt = cdiv(e.m, info.tile_m);

@@ -80,7 +80,7 @@ int sm_count() {
     return sms;
 }
 
-gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o) {
+gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o, bool tma) {
     const bool small_tile = o.tile == 64 || (o.tile == 0 && (nest.m_r < 128 || nest.n_r < 128));
     if (o.tile != 0 && o.tile != 64 && o.tile != 128) fail_usage("tile must be 0, 64 or 128");
     const int tn = o.tile_n == 0 ? o.tile : o.tile_n;
@@ -89,9 +89,12 @@ gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o) {
     switch (o.numerics) {
         case TM_NUMERICS_DMMA:
             if (o.tile == 128 && tn == 64) return gpu::kDmma128x64;
-            // short k: every task is mostly C load/store; two CTAs per SM
-            // (128 x 64 tiles) hide one CTA's C traffic behind the other's DMMAs
-            if (o.tile == 0 && !small_tile && nest.ext.k <= 512 && o.schedule == TM_SCHEDULE_FUSED)
+            // short k: every task is mostly C load/store. With TMA staging the
+            // 128 x 128 kernel's producer loads the next tile's first slabs
+            // under this tile's C write-back (rank-k 16384^2 x 256: 87.3 % of
+            // peak); with cp.async, two CTAs per SM (128 x 64 tiles) hide one
+            // CTA's C traffic behind the other's DMMAs (84.1 %).
+            if (o.tile == 0 && !small_tile && nest.ext.k <= 512 && o.schedule == TM_SCHEDULE_FUSED && !tma)
                 return gpu::kDmma128x64;
             return small_tile ? gpu::kDmma64 : gpu::kDmma128;
         case TM_NUMERICS_FMA:
@@ -481,7 +484,9 @@ void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t l
     if (lda < e.m || ldb < e.k || ldc < e.m) fail_usage("leading dimension smaller than the operand's row count");
     tm_exec_opts o{};
     if (opts) o = *opts;
-    const gpu::Kernel kernel = pick_kernel(plan->nest, o);
+    const bool tma_hint = o.staging != TM_STAGING_CPASYNC && lda % 2 == 0 && ldb % 2 == 0 &&
+                          reinterpret_cast<uintptr_t>(A) % 16 == 0 && reinterpret_cast<uintptr_t>(B) % 16 == 0;
+    const gpu::Kernel kernel = pick_kernel(plan->nest, o, tma_hint);
     std::lock_guard<std::mutex> lk(plan->mu);
     Key key{o.schedule, kernel, o.schedule == TM_SCHEDULE_FUSED ? o.split_k : 0, o.ctas, false,
             o.schedule == TM_SCHEDULE_FAITHFUL ? o.parallel_loop : 0};
