@@ -126,7 +126,7 @@ def cmd_run(a) -> int:
     A, B = T.fill_seeded(a.seed, [(shape.m, shape.k), (shape.k, shape.n)])  # tilemul_main.cpp:236-242
     dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
     dC = torch.zeros(shape.m * shape.n, dtype=torch.float64, device="cuda")
-    opts = T.ExecOptions(numerics=a.numerics, schedule=a.schedule)
+    opts = T.ExecOptions(numerics=a.numerics, schedule=a.schedule, staging=a.staging)
     T.execute(nest, dA, dB, dC.clone(), opts)  # warm: lowering + module load outside the timed window
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -324,6 +324,8 @@ def main(argv=None) -> int:
             p.add_argument("--verify-max", dest="verify_max", type=int, default=1 << 27)
             p.add_argument("--numerics", default="dmma", choices=["dmma", "fma", "exact"])
             p.add_argument("--schedule", default="fused", choices=["fused", "faithful"])
+            p.add_argument("--staging", default="auto", choices=["auto", "cpasync", "tma"],
+                           help="DMMA kernels: how A/B k-slabs reach shared memory (auto: by measured evidence)")
             p.add_argument("--colmajor", action="store_true", help="accepted; the GPU path is column-major")
         if name == "simulate":
             p.add_argument("--trace-dump", dest="trace_dump", help="write the plain-text trace to a file")
