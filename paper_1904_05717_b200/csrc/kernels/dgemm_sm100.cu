@@ -24,6 +24,8 @@
 //                 across task boundaries (the next task's first slabs land
 //                 under this task's epilogue).
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include <cuda.h>
@@ -555,7 +557,8 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, uin
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool FIX = true>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
-    k_dmma_tma(Args a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+    k_dmma_tma(Args a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmC) {
     constexpr int NWM = BM / WM, NW = (BM / WM) * (BN / WN);
     constexpr int FM = WM / 8, FN = WN / 8, KK = BK / 4;
     constexpr int PD = STAGES - 1;
@@ -617,6 +620,13 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
             pc.j0 = pt.j0;
             pc.p0 = pt.p0;
             pc.ready = pt.ready;
+            if (a.prefetch_c && pt.slice < 0 && pt.ready == 0 && pc.issued > 0) {  // (not the CTA's first task)
+                // the tile's C is read at the task's start, about two slabs from now: warm L2 with it
+                asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                                 reinterpret_cast<uint64_t>(&tmC)),
+                             "r"(pt.i0), "r"(pt.j0)
+                             : "memory");
+            }
             break;
         }
         pc.ti = x;
@@ -996,7 +1006,8 @@ cudaError_t launch_tma(Kernel kernel, const Args& args, int64_t M, int64_t N, in
     if (args.ntasks <= 0) return cudaSuccess;
     auto* encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
     if (encode == nullptr) return cudaErrorNotSupported;
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, mc;
+    std::memset(&mc, 0, sizeof(mc));
     const cuuint32_t estr[2] = {1, 1};
     {
         const cuuint64_t dims[2] = {static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(K)};
@@ -1016,8 +1027,20 @@ cudaError_t launch_tma(Kernel kernel, const Args& args, int64_t M, int64_t N, in
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
+    bool cmap = false;
+    if (!(args.ldc & 1) && !(reinterpret_cast<uintptr_t>(args.C) & 15)) {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(N)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(args.ldc) * 8};
+        // one box = one C tile (prefetch only, so no swizzle constraint on the inner extent)
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTable[kernel].tile_m), static_cast<cuuint32_t>(en.box_n)};
+        cmap = encode(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, args.C, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     Args local = args;
-    void* params[] = {&local, &ma, &mb};
+    local.prefetch_c = cmap ? 1 : 0;
+    if (const char* env = std::getenv("TILEMUL_TMA_PREFETCH_C")) local.prefetch_c &= std::atoi(env);
+    void* params[] = {&local, &ma, &mb, &mc};
     return cudaLaunchKernel(en.fn, dim3(grid), dim3(kTable[kernel].threads), params, en.smem, stream);
 }
 

@@ -54,6 +54,7 @@ struct Args {
                                // nullptr = strided (task t on CTA t mod grid)
     const int32_t* ready;      // data flags written by the copy stream (Task::ready), or nullptr
     int32_t* done;             // per-block completion counters (Task::done), or nullptr
+    int32_t prefetch_c = 0;    // TMA kernels: warm L2 with each task's C tile when the producer reaches it
 };
 
 // One k-split C tile: its partials live in slots slot0 .. slot0+nslots-1 and
