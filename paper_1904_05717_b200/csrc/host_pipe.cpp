@@ -345,6 +345,7 @@ void execute_host(tm_plan* plan, const double* A, const double* B, double* C, co
             tasks += pq->last_tasks;
             launches += pq->last_launches;
             ctas = pq->last_ctas;
+            plan->last_staging = pq->last_staging;
             for (int f : finished) d2h(f);
             finished.clear();
             if (q == nq - 1) {
