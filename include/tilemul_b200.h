@@ -90,7 +90,8 @@ typedef struct {
     int32_t ctas;       /* persistent grid size (0 = SMs x occupancy) */
     int32_t tile;       /* CTA tile rows: 128 or 64 (0 = auto from the register tile); tensor-core path:
                            128 = one SM (cta_group::1), 0/256 = an SM pair (cta_group::2) */
-    int32_t tile_n;     /* CTA tile columns (0 = same as tile); 128 x 64 runs two CTAs per SM */
+    int32_t tile_n;     /* CTA tile columns (0 = same as tile); 128 x 64 runs two CTAs per SM; tensor-core
+                           SM pairs: 512 (the default, 0) or 256 */
     /* Faithful schedule: the m/n loop whose iterations run as independent
      * workers (ExecOptions::parallel_loop, exec.hpp:50-53, :125-131), as
      * loop index + 1; 0 = plain nest order (consecutive cells on the CTAs,

@@ -292,9 +292,16 @@ int tm_execute_tc(tm_plan* plan, int dtype, const void* A, int64_t lda, const vo
         if (o.split_k > 1) fail_usage("tensor-core path does not split k");
         o.split_k = 1;
         if (o.tile != 0 && o.tile != 128 && o.tile != 256) fail_usage("tensor-core tile must be 128 (1 SM) or 256 (SM pair)");
+        if (o.tile_n != 0 && o.tile_n != 256 && o.tile_n != 512) fail_usage("tensor-core tile_n must be 256 or 512");
         const bool pair = o.tile != 128;
-        const gpu::Kernel kernel = dtype == TM_DTYPE_TF32 ? (pair ? gpu::kTc2Tf32 : gpu::kTcTf32)
-                                                          : (pair ? gpu::kTc2Bf16 : gpu::kTcBf16);
+        if (!pair && o.tile_n == 512) fail_usage("512-column tiles run on SM pairs only");
+        // SM pairs default to 256 x 512 tiles: 25 % fewer L2->SMEM bytes per flop than 256 x 256, which
+        // under the board power cap buys clock (config 4)
+        const bool wide = pair && o.tile_n != 256;
+        const bool tf32 = dtype == TM_DTYPE_TF32;
+        const gpu::Kernel kernel = wide   ? (tf32 ? gpu::kTc2wTf32 : gpu::kTc2wBf16)
+                                   : pair ? (tf32 ? gpu::kTc2Tf32 : gpu::kTc2Bf16)
+                                          : (tf32 ? gpu::kTcTf32 : gpu::kTcBf16);
         std::lock_guard<std::mutex> lk(plan->mu);
         Key key{o.schedule, kernel, 1, o.ctas, false};
         auto& slot = plan->schedules[key];
@@ -304,7 +311,7 @@ int tm_execute_tc(tm_plan* plan, int dtype, const void* A, int64_t lda, const vo
         Schedule& s = *slot;
         const int nt = static_cast<int>(s.host_tasks.size());
         cuda_check(pair ? gpu::launch_tc_pair(dtype == TM_DTYPE_TF32, A, lda, B, ldb, C, ldc, e.m, e.n, e.k, s.tasks,
-                                              nt, s.grid, static_cast<cudaStream_t>(stream))
+                                              nt, s.grid, static_cast<cudaStream_t>(stream), wide)
                         : gpu::launch_tc(dtype == TM_DTYPE_TF32, A, lda, B, ldb, C, ldc, e.m, e.n, e.k, s.tasks, nt,
                                          s.grid, static_cast<cudaStream_t>(stream)),
                    "tensor-core kernel launch (TMA needs 16-byte aligned bases and leading dimensions)");

@@ -75,7 +75,9 @@ enum Kernel : int {
     kTcBf16 = 100,    // tcgen05 BF16 inputs, fp32 TMEM accumulate, 128x256 tile (tc_gemm_sm100.cu)
     kTcTf32 = 101,    // tcgen05 TF32 inputs
     kTc2Bf16 = 102,   // tcgen05.mma.cta_group::2: 2-CTA cluster, 256x256 tile per pair
-    kTc2Tf32 = 103
+    kTc2Tf32 = 103,
+    kTc2wBf16 = 104,  // 2-CTA cluster, 256x512 tile per pair (25 % fewer L2->SMEM bytes per flop)
+    kTc2wTf32 = 105
 };
 
 struct KernelInfo {
@@ -116,11 +118,12 @@ cudaError_t launch_tc(bool tf32, const void* A, int64_t lda, const void* B, int6
 // fp64 -> bf16 (RNE) or fp64 -> tf32-valued fp32 (RNE to 11 significant bits).
 cudaError_t launch_round(bool tf32, const double* x, void* y, int64_t count, cudaStream_t stream);
 int tc_smem_bytes(bool tf32);
-// Same contract, 2-SM pair kernel: tasks are 256 x 256 tiles, grid even (clusters of 2).
+// Same contract, 2-SM pair kernel: tasks are 256 x 256 tiles (wide: 256 x
+// 512, one TMEM accumulator of 512 columns), grid even (clusters of 2).
 cudaError_t launch_tc_pair(bool tf32, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                            int64_t m, int64_t n, int64_t k, const Task* tasks, int ntasks, int grid,
-                           cudaStream_t stream);
-int tc2_smem_bytes(bool tf32);
+                           cudaStream_t stream, bool wide = false);
+int tc2_smem_bytes(bool tf32, bool wide = false);
 // A hierarchical layout for the relayout kernel (<= kMaxCuts partition steps).
 struct LayoutDev {
     static constexpr int kMaxCuts = 24;

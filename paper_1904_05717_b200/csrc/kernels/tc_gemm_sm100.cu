@@ -18,6 +18,8 @@
 // The SMEM level of the MOMMS member is the TMA ring; the register level is
 // the TMEM accumulator (128 x 256 fp32 per tile).
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include <cuda.h>
@@ -434,7 +436,11 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
         : "memory");
 }
 
-template <bool TF32>
+// NH = 256-column halves of the pair tile: 1 -> 256 x 256 per pair, two
+// TMEM accumulators (the next tile's MMAs overlap this tile's epilogue);
+// 2 -> 256 x 512 per pair, one accumulator filling TMEM (512 columns), 25 %
+// fewer L2->SMEM bytes per flop, epilogue by 8 warps and not overlapped.
+template <bool TF32, int NH = 1>
 struct Tc2Geo {
     static constexpr int E = TF32 ? 4 : 2;
     static constexpr int BK = 128 / E;
@@ -442,12 +448,16 @@ struct Tc2Geo {
     static constexpr int A_BOXES = 128 / MATOM;  // this CTA's 128 rows
     static constexpr int A_BOX_BYTES = 128 * BK;
     static constexpr int A_BYTES = 128 * BK * E;
-    static constexpr int B_BYTES = 128 * BK * E;  // this CTA's 128 columns
+    static constexpr int B_HALF_BYTES = 128 * BK * E;  // this CTA's 128 columns of one 256-column half
+    static constexpr int B_BYTES = NH * B_HALF_BYTES;
     static constexpr int STAGE = A_BYTES + B_BYTES;
     static constexpr int PAIR_STAGE_BYTES = 2 * STAGE;
     static constexpr int UK = 32 / E;
     static constexpr int NMMA = BK / UK;
-    static constexpr int STAGES = 6;
+    static constexpr int STAGES = NH == 1 ? 6 : 4;
+    static constexpr int NACC = NH == 1 ? 2 : 1;      // TMEM accumulators of 256 * NH columns
+    static constexpr int EPI_WARPS = 4 * NH;
+    static constexpr int THREADS = 128 + 32 * EPI_WARPS;
     static constexpr uint32_t A_LAYOUT = TF32 ? 1u : 2u;
     static constexpr uint32_t A_SBO = TF32 ? 512u : 1024u;
     static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
@@ -459,10 +469,10 @@ __host__ __device__ constexpr uint32_t instr_desc_pair() {
            (static_cast<uint32_t>(256 >> 3) << 17) | (static_cast<uint32_t>(256 >> 4) << 24);
 }
 
-template <bool TF32>
-__global__ void __launch_bounds__(256, 1) k_tc2(const __grid_constant__ CUtensorMap tmA,
-                                                const __grid_constant__ CUtensorMap tmB, TcArgs a) {
-    using G = Tc2Geo<TF32>;
+template <bool TF32, int NH = 1>
+__global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __grid_constant__ CUtensorMap tmA,
+                                                                  const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+    using G = Tc2Geo<TF32, NH>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::STAGES * G::STAGE);
@@ -487,7 +497,7 @@ __global__ void __launch_bounds__(256, 1) k_tc2(const __grid_constant__ CUtensor
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 8);
+            mbar_init(&tempty[s], 2 * G::EPI_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -519,7 +529,10 @@ __global__ void __launch_bounds__(256, 1) k_tc2(const __grid_constant__ CUtensor
                     for (int h = 0; h < G::A_BOXES; ++h)
                         tma_load_2d_pair(sa + h * G::A_BOX_BYTES, &tmA, bar,
                                          t.i0 + static_cast<int>(rank) * 128 + h * G::MATOM, kc);
-                    tma_load_2d_pair(sb, &tmB, bar, kc, t.j0 + static_cast<int>(rank) * 128);
+#pragma unroll
+                    for (int h = 0; h < NH; ++h)
+                        tma_load_2d_pair(sb + h * G::B_HALF_BYTES, &tmB, bar, kc,
+                                         t.j0 + h * 256 + static_cast<int>(rank) * 128);
                     if (++stage == G::STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -548,8 +561,11 @@ __global__ void __launch_bounds__(256, 1) k_tc2(const __grid_constant__ CUtensor
 #pragma unroll
                     for (int kk = 0; kk < G::NMMA; ++kk) {
                         const uint64_t da = smem_desc(sa + kk * G::UK * 128, G::A_BOX_BYTES, G::A_SBO, G::A_LAYOUT);
-                        const uint64_t db = smem_desc(sb + kk * 32, 16, 1024);
-                        umma_pair<TF32>(tmem_d, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+#pragma unroll
+                        for (int h = 0; h < NH; ++h) {
+                            const uint64_t db = smem_desc(sb + h * G::B_HALF_BYTES + kk * 32, 16, 1024);
+                            umma_pair<TF32>(tmem_d + h * 256, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        }
                     }
                     umma_commit_pair(&empty[stage]);
                     if (++stage == G::STAGES) {
@@ -558,14 +574,14 @@ __global__ void __launch_bounds__(256, 1) k_tc2(const __grid_constant__ CUtensor
                     }
                 }
                 umma_commit_pair(&tfull[acc]);
-                if (++acc == 2) {
+                if (++acc == G::NACC) {
                     acc = 0;
                     aphase ^= 1;
                 }
             }
         }
-    } else if (warp >= 4) {  // ---------------- epilogue (both CTAs, own 128 rows)
-        const int ew = warp - 4;
+    } else if (warp >= 4) {  // ---------------- epilogue (both CTAs, own 128 rows; warp group h: columns of half h)
+        const int ew = warp & 3, h = (warp - 4) >> 2;  // TMEM lanes 32*(warp%4).. are this warp's
         const int row = static_cast<int>(rank) * 128 + ew * 32 + lane;
         int acc = 0;
         uint32_t aphase = 0;
@@ -574,20 +590,20 @@ __global__ void __launch_bounds__(256, 1) k_tc2(const __grid_constant__ CUtensor
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
             const bool live = row < t.m;
-            float* crow = a.C + (static_cast<int64_t>(t.i0) + row) + static_cast<int64_t>(t.j0) * a.ldc;
+            float* crow = a.C + (static_cast<int64_t>(t.i0) + row) + static_cast<int64_t>(t.j0 + h * 256) * a.ldc;
 #pragma unroll 1
             for (int cb = 0; cb < 256 / 32; ++cb) {
                 uint32_t r[32];
                 const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) +
-                                       static_cast<uint32_t>(acc * 256 + cb * 32);
+                                       static_cast<uint32_t>(acc * 256 + h * 256 + cb * 32);
                 TC_LD32(taddr, r);
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                if (live) epilogue_chunk(crow + static_cast<int64_t>(cb * 32) * a.ldc, a.ldc, t.n - cb * 32, r);
+                if (live) epilogue_chunk(crow + static_cast<int64_t>(cb * 32) * a.ldc, a.ldc, t.n - h * 256 - cb * 32, r);
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(mapa_rank(&tempty[acc], 0));
-            if (++acc == 2) {
+            if (++acc == G::NACC) {
                 acc = 0;
                 aphase ^= 1;
             }
@@ -684,10 +700,10 @@ __global__ void k_round_tf32(const double* x, float* y, int64_t count) {
     }
 }
 
-template <bool TF32>
+template <bool TF32, int NH>
 cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc, int64_t m,
                          int64_t n, int64_t k, const Task* tasks, int ntasks, int grid, cudaStream_t stream) {
-    using G = Tc2Geo<TF32>;
+    using G = Tc2Geo<TF32, NH>;
     cudaError_t e = encoder();
     if (e != cudaSuccess) return e;
     if ((lda * G::E) % 16 || (ldb * G::E) % 16 || reinterpret_cast<uintptr_t>(A) % 16 ||
@@ -701,7 +717,7 @@ cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb,
     static bool attr[2] = {false, false};
     std::lock_guard<std::mutex> lk(g_tc_mu);
     if (!attr[TF32]) {
-        if ((e = cudaFuncSetAttribute(k_tc2<TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM)) !=
+        if ((e = cudaFuncSetAttribute(k_tc2<TF32, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM)) !=
             cudaSuccess)
             return e;
         attr[TF32] = true;
@@ -709,7 +725,7 @@ cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb,
     TcArgs args{C, ldc, tasks, ntasks};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(G::THREADS);
     cfg.dynamicSmemBytes = G::SMEM;
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
@@ -719,20 +735,26 @@ cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb,
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_tc2<TF32>, ma, mb, args);
+    return cudaLaunchKernelEx(&cfg, k_tc2<TF32, NH>, ma, mb, args);
 }
 
 }  // namespace
 
 cudaError_t launch_tc_pair(bool tf32, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                            int64_t m, int64_t n, int64_t k, const Task* tasks, int ntasks, int grid,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, bool wide) {
     if (ntasks <= 0) return cudaSuccess;
-    return tf32 ? launch_tc2_t<true>(A, lda, B, ldb, C, ldc, m, n, k, tasks, ntasks, grid, stream)
-                : launch_tc2_t<false>(A, lda, B, ldb, C, ldc, m, n, k, tasks, ntasks, grid, stream);
+    if (wide)
+        return tf32 ? launch_tc2_t<true, 2>(A, lda, B, ldb, C, ldc, m, n, k, tasks, ntasks, grid, stream)
+                    : launch_tc2_t<false, 2>(A, lda, B, ldb, C, ldc, m, n, k, tasks, ntasks, grid, stream);
+    return tf32 ? launch_tc2_t<true, 1>(A, lda, B, ldb, C, ldc, m, n, k, tasks, ntasks, grid, stream)
+                : launch_tc2_t<false, 1>(A, lda, B, ldb, C, ldc, m, n, k, tasks, ntasks, grid, stream);
 }
 
-int tc2_smem_bytes(bool tf32) { return tf32 ? Tc2Geo<true>::SMEM : Tc2Geo<false>::SMEM; }
+int tc2_smem_bytes(bool tf32, bool wide) {
+    return wide ? (tf32 ? Tc2Geo<true, 2>::SMEM : Tc2Geo<false, 2>::SMEM)
+                : (tf32 ? Tc2Geo<true, 1>::SMEM : Tc2Geo<false, 1>::SMEM);
+}
 
 cudaError_t launch_tc(bool tf32, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,
                       int64_t m, int64_t n, int64_t k, const Task* tasks, int ntasks, int grid, cudaStream_t stream) {

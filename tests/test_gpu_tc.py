@@ -16,17 +16,21 @@ pytestmark = pytest.mark.gpu
 U32 = 2.0 ** -24
 
 
-def tc_plan(m, n, k, tile=128):
-    # register tile = the TMEM accumulator (128 x 256 fp32); capacities in 2-byte elements
-    hier = T.CacheHierarchy.from_capacities([128 * 512, 232448 // 2, 132644864 // 2])
+def tc_plan(m, n, k, tile=128, tile_n=256):
+    # register tile = the TMEM accumulator (128 x 256 fp32; 256 x 512 over an SM pair for the wide
+    # tile, whose SMEM level is then the pair's); capacities in 2-byte elements
+    if tile_n == 512:
+        hier = T.CacheHierarchy.from_capacities([256 * 512, 232448, 132644864 // 2])
+    else:
+        hier = T.CacheHierarchy.from_capacities([128 * 512, 232448 // 2, 132644864 // 2])
     d = T.parse_name("C2A1C0")
-    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(tile, 256)),
+    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(tile, tile_n)),
                              pinned=T.BlocksizeSet({(1, "m"): min(tile, m)}))
     return T.build_plan(d, bs, hier, T.Shape(m, n, k))
 
 
-def run_case(m, n, k, dtype, sample=None, seed=5, tile=0):
-    nest = tc_plan(m, n, k, tile if tile else 256)
+def run_case(m, n, k, dtype, sample=None, seed=5, tile=0, tile_n=0):
+    nest = tc_plan(m, n, k, tile if tile else 256, tile_n or (512 if tile != 128 else 256))
     A64 = torch.empty(m * k, dtype=torch.float64, device="cuda")
     B64 = torch.empty(k * n, dtype=torch.float64, device="cuda")
     T.fill_uniform_device(A64, seed)
@@ -37,7 +41,7 @@ def run_case(m, n, k, dtype, sample=None, seed=5, tile=0):
     T.fill_uniform_device(C0, seed + 2)
     C = C0.float()
     c0 = C.double().cpu().numpy()
-    T.execute_tc(nest, A, B, C, dtype, T.ExecOptions(tile=tile))
+    T.execute_tc(nest, A, B, C, dtype, T.ExecOptions(tile=tile, tile_n=tile_n))
     torch.cuda.synchronize()
     got = C.double().cpu().numpy()
     a = A.double().cpu().numpy()
@@ -59,18 +63,23 @@ def run_case(m, n, k, dtype, sample=None, seed=5, tile=0):
     return nest
 
 
-@pytest.mark.parametrize("tile", [128, 256])  # one SM (cta_group::1) / SM pair (cta_group::2)
-@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
-@pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 1024), (136, 264, 520), (1000, 776, 328)])
-def test_tc_small_full_check(dtype, shape, tile):
-    run_case(*shape, dtype, tile=tile)
+# one SM (cta_group::1) / SM pair (cta_group::2) 256x256 / SM pair 256x512 (one 512-column TMEM accumulator)
+TILES = [(128, 0), (256, 256), (256, 0)]  # (256, 0): the default, 256 x 512 per pair
 
 
-@pytest.mark.parametrize("tile", [128, 256])
+@pytest.mark.parametrize("tile,tile_n", TILES)
 @pytest.mark.parametrize("dtype", ["bf16", "tf32"])
-def test_tc_large_sampled(dtype, tile):
-    nest = run_case(4096, 4096, 4096, dtype, sample=2048, tile=tile)
-    assert nest.last_launch()["tasks"] == (4096 // tile) * (4096 // 256)
+@pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 1024), (136, 264, 520), (1000, 776, 328),
+                                   (304, 1104, 208)])
+def test_tc_small_full_check(dtype, shape, tile, tile_n):
+    run_case(*shape, dtype, tile=tile, tile_n=tile_n)
+
+
+@pytest.mark.parametrize("tile,tile_n", TILES)
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_tc_large_sampled(dtype, tile, tile_n):
+    nest = run_case(4096, 4096, 4096, dtype, sample=2048, tile=tile, tile_n=tile_n)
+    assert nest.last_launch()["tasks"] == (4096 // tile) * (4096 // (tile_n or (512 if tile == 256 else 256)))
 
 
 def test_tc_rejects_unaligned_and_faithful():

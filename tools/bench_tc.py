@@ -28,11 +28,15 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
     m = n = k = size
-    hier = T.CacheHierarchy.from_capacities([128 * 512, 232448 // 2, 132644864 // 2])
+    hier1 = T.CacheHierarchy.from_capacities([128 * 512, 232448 // 2, 132644864 // 2])
+    hier2 = T.CacheHierarchy.from_capacities([256 * 512, 232448, 132644864 // 2])  # 256x512 over an SM pair
     d = T.parse_name("C2A1C0")
-    def plan(tile):
-        bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(tile, 256)),
-                                 pinned=T.BlocksizeSet({(1, "m"): tile, (2, "m"): L2M, (2, "n"): L2N}))
+    def plan(tile, tile_n=256):
+        # one wave of pair tiles per L2 block: 6 x 12 of 256 x 256, 8 x 9 of 256 x 512
+        l2m, l2n = (L2M, L2N) if tile_n == 256 else (2048, 4608)
+        hier = hier1 if tile_n == 256 else hier2
+        bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(tile, tile_n)),
+                                 pinned=T.BlocksizeSet({(1, "m"): tile, (2, "m"): l2m, (2, "n"): l2n}))
         return T.build_plan(d, bs, hier, T.Shape(m, n, k)), bs
 
     A64 = torch.empty(m * k, dtype=torch.float64, device="cuda")
@@ -42,14 +46,14 @@ def main():
     # live tcgen05 issue-rate peaks: bursts at full clocks, and ~200 ms launches under the power cap
     probe = {dt: T.measure_tc_peak(dt, 10) for dt in ("bf16", "tf32")}
     probe_sus = {dt: T.measure_tc_peak(dt, 3, sustained=True) for dt in ("bf16", "tf32")}
-    cases = os.environ.get("TC_CASES", "bf16:256,bf16:128,tf32:256,tf32:128").split(",")
-    for dtype, tile in ((c.split(":")[0], int(c.split(":")[1])) for c in cases):
-        nest, bs = plan(tile)
+    cases = os.environ.get("TC_CASES", "bf16:256:512,bf16:256:256,bf16:128,tf32:256:512,tf32:256:256,tf32:128").split(",")
+    for dtype, tile, tile_n in ((c.split(":")[0], int(c.split(":")[1]), int((c.split(":") + ["256"])[2])) for c in cases):
+        nest, bs = plan(tile, tile_n)
         A = T.round_inputs(A64, dtype)
         B = T.round_inputs(B64, dtype)
         C = torch.zeros(m * n, dtype=torch.float32, device="cuda")
         for _ in range(2):
-            T.execute_tc(nest, A, B, C, dtype, T.ExecOptions(tile=tile))
+            T.execute_tc(nest, A, B, C, dtype, T.ExecOptions(tile=tile, tile_n=tile_n))
         torch.cuda.synchronize()
         ts = []
         import bench
@@ -58,7 +62,7 @@ def main():
         for _ in range(40):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            T.execute_tc(nest, A, B, C, dtype, T.ExecOptions(tile=tile))
+            T.execute_tc(nest, A, B, C, dtype, T.ExecOptions(tile=tile, tile_n=tile_n))
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e-3)
@@ -75,7 +79,7 @@ def main():
                                           "(cta_group::1), same clocks/power state as this run",
                           "frac_of_sustained": tf / (peaks.get("bf16_tflops_sustained", peak * 2) /
                                                     (1 if dtype == "bf16" else 2)),
-                          "cta_tile": "256x256 per SM pair (cta_group::2)" if tile == 256 else "128x256 (cta_group::1)",
+                          "cta_tile": (f"256x{tile_n} per SM pair (cta_group::2)" if tile == 256 else "128x256 (cta_group::1)"),
                           "blocksizes": {f"{lv}:{dd}": v for (lv, dd), v in bs.entries()},
                           "launch": nest.last_launch(), "clocks": clk.summary()}), flush=True)
         del A, B, C
