@@ -16,14 +16,24 @@ column (NCCL, on NCCL's stream) while the local GEMM of chunk j-1 runs on
 the compute stream; k is never split across ranks, so there is no reduction
 and every C entry still accumulates in ascending k.
 
-The data movement is plain torch.distributed (NCCL on GPUs, gloo in the CPU
-tests); the local GEMM is `tilemul.execute` on the sm_100a task kernel. The
-`gemm` hook exists so the CPU tests can drive the same schedule with a
-host matmul — the product path always passes the native GEMM.
+The data movement is either torch.distributed broadcasts (NCCL on GPUs, gloo
+in the CPU tests) or, with exchange="ce", copy-engine pulls over peer memory:
+every rank maps its row peers' A pieces and column peers' B pieces once
+(CUDA IPC handles, exchanged over the process group), and chunk j+1 is
+copied peer -> local receive buffer by the DMA engines on a side stream while
+chunk j's GEMM runs. NCCL's broadcast kernels need SMs, which the local
+GEMM's persistent grid holds entirely, so they can only run between GEMMs;
+the copy engines need none. The pieces a rank maps must not change while
+peers read them (the device-resident bench path; the e2e path, which uploads
+per step, keeps the broadcasts). The local GEMM is `tilemul.execute` on the
+sm_100a task kernel. The `gemm` hook exists so the CPU tests can drive the
+same schedule with a host matmul — the product path always passes the
+native GEMM.
 """
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from typing import Callable, Optional, Tuple
 
@@ -95,6 +105,8 @@ class Summa:
         self.r, self.c = lay.coords(rank)
         self.dist = dist
         self.row_group, self.col_group = row_group, col_group
+        self.peer_a = self.peer_b = None  # exchange="ce": peers' A pieces by column, B pieces by row
+        self.ce_stream = None
         # receive buffers only where chunks actually arrive from peers
         self.abuf = [torch.empty(lay.mL * lay.KC, dtype=torch.float64, device=device)
                      for _ in range(2 if lay.Pc > 1 else 0)]
@@ -109,6 +121,34 @@ class Summa:
         cols = [dist.new_group([lay.rank_of(r, c) for r in range(lay.Pr)]) for c in range(lay.Pc)]
         return rows, cols
 
+    def attach_peers(self, A_local, B_local) -> None:
+        """Copy-engine exchange: map every row peer's A pieces and column
+        peer's B pieces (CUDA IPC; all ranks must call, after filling their
+        pieces). The pieces must stay unchanged while peers read them."""
+        import torch
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        lay = self.lay
+        mine = (reduce_tensor(A_local), reduce_tensor(B_local))
+        allh = [None] * (lay.Pr * lay.Pc)
+        self.dist.all_gather_object(allh, mine)
+        self.peer_a, self.peer_b = {}, {}
+        for c in range(lay.Pc):
+            if c != self.c:
+                fn, args = allh[lay.rank_of(self.r, c)][0]
+                self.peer_a[c] = fn(*args)
+        for r in range(lay.Pr):
+            if r != self.r:
+                fn, args = allh[lay.rank_of(r, self.c)][1]
+                self.peer_b[r] = fn(*args)
+        self.ce_stream = torch.cuda.Stream(device=self.device)
+        self.dist.barrier()  # every rank holds its peers' mappings before any rank frees or reuses its pieces
+
+    def detach_peers(self) -> None:
+        """Back to the broadcasts (collective: call on every rank)."""
+        self.dist.barrier()  # no rank still pulls from a peer whose pieces are about to change
+        self.peer_a = self.peer_b = None
+
     def a_chunk_view(self, A_local, j: int):
         lay = self.lay
         q = lay.a_local_chunk(j)
@@ -119,8 +159,34 @@ class Summa:
         q = lay.b_local_chunk(j)
         return B_local[q * lay.KC * lay.nL:(q + 1) * lay.KC * lay.nL]
 
+    def _pull(self, A_local, B_local, j: int):
+        """Copy-engine pulls of chunk j from the owners' memory into the
+        receive buffers, on the side stream; returns (a, b, works)."""
+        import torch
+
+        lay = self.lay
+        a_src_c, b_src_r = lay.a_owner(j), lay.b_owner(j)
+        a = self.a_chunk_view(A_local, j) if a_src_c == self.c else self.abuf[j % 2]
+        b = self.b_chunk_view(B_local, j) if b_src_r == self.r else self.bbuf[j % 2]
+        if a_src_c == self.c and b_src_r == self.r:
+            return a, b, []
+        st = self.ce_stream
+        st.wait_stream(torch.cuda.current_stream(self.device))  # the buffer's last reader (GEMM j-2) is queued there
+        with torch.cuda.stream(st):
+            if a_src_c != self.c:
+                a.copy_(self.a_chunk_view(self.peer_a[a_src_c], j), non_blocking=True)
+                self.exchanged_bytes += a.numel() * 8
+            if b_src_r != self.r:
+                b.copy_(self.b_chunk_view(self.peer_b[b_src_r], j), non_blocking=True)
+                self.exchanged_bytes += b.numel() * 8
+            ev = torch.cuda.Event()
+            ev.record(st)
+        return a, b, [_StreamWait(ev, self.device)]
+
     def _post(self, A_local, B_local, j: int):
         """Issue the broadcasts of chunk j; returns (a, b, works)."""
+        if self.peer_a is not None:
+            return self._pull(A_local, B_local, j)
         lay = self.lay
         works = []
         a_src_c, b_src_r = lay.a_owner(j), lay.b_owner(j)
@@ -148,6 +214,8 @@ class Summa:
         last read by the GEMM two chunks back), so uploads, exchanges and
         GEMMs overlap."""
         L = self.lay.chunks
+        if ready is not None and self.peer_a is not None:
+            raise ValueError("copy-engine pulls read the peers' pieces in place: per-step uploads need the broadcasts")
         cur = None
         if comm is not None:
             import torch
@@ -175,6 +243,19 @@ class Summa:
             if j + 1 < L:
                 pending = post(j + 1)  # overlaps the GEMM below
             self.gemm(a, b, C_local)
+
+
+class _StreamWait:
+    """A copy-engine pull's completion, waited like a collective's Work:
+    the compute stream waits on the side stream's event."""
+
+    def __init__(self, ev, device):
+        self.ev, self.device = ev, device
+
+    def wait(self):
+        import torch
+
+        torch.cuda.current_stream(self.device).wait_event(self.ev)
 
 
 def fill_local(lay: Layout, rank: int, A_local, B_local, C_local, fill_block, seeds=(11, 12, 13)):
@@ -223,6 +304,15 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
         T.execute(nest, a, b, cc, opts)
 
     s = Summa(lay, rank, dev, gemm, dist, rows[r], cols[c])
+    exchange = "nccl broadcasts"
+    if world > 1 and os.environ.get("TILEMUL_EXCHANGE", "ce") == "ce":
+        try:  # copy-engine pulls over peer memory; the broadcasts if the peers cannot be mapped
+            s.attach_peers(A, B)
+            exchange = "copy-engine pulls over CUDA IPC peer mappings"
+        except Exception as exc:  # noqa: BLE001
+            exchange = f"nccl broadcasts (peer mapping failed: {type(exc).__name__})"
+            s.peer_a = s.peer_b = None
+            dist.barrier()
     for _ in range(args.warmup):
         s.run(A, B, C)
     torch.cuda.synchronize()
@@ -245,6 +335,8 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
     per_gpu = flops / world / t / 1e12
 
     e2e = None
+    if s.peer_a is not None:
+        s.detach_peers()  # the e2e step re-uploads the pieces every step: broadcasts
     if not args.no_e2e:
         Ah, Bh, Ch = (x.cpu().pin_memory() for x in (A, B, C))
         steps = max(1, min(args.steps, 3))
@@ -301,6 +393,7 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
             "config": {"workload": f"fp64 C+=A*B, C 2-D partitioned {lay.Pr}x{lay.Pc}, local {lay.mL}x{lay.nL}, "
                                    f"K={lay.K}, family C2A1C0 fused/DMMA", "grid": [lay.Pr, lay.Pc],
                        "chunks": lay.chunks, "kc": lay.KC, "parallelism": f"2-D C partition {lay.Pr}x{lay.Pc}",
+                       "exchange": exchange,
                        "l2_flush": "not needed: per-rank inputs >> 126 MB L2"},
             "pct_of_fp64_peak_per_gpu": 100.0 * per_gpu / peak,
             "roofline": {"bound": "tensor", "achieved": per_gpu, "peak": peak, "unit": "TFLOP/s",

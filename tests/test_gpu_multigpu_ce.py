@@ -1,0 +1,114 @@
+"""The multi-GPU driver's copy-engine exchange (multigpu.Summa.attach_peers:
+peer pieces mapped over CUDA IPC, chunks pulled by the DMA engines under the
+local GEMM) with the sm_100a kernel as the local GEMM.
+
+This box has one GPU, so the ranks are 2 and 4 processes sharing cuda:0
+with gloo as the control plane (handle exchange, barriers). Nothing here
+makes one rank's kernel wait on another's: the pulls read pieces that are
+static after the fill, so sharing the device changes timing, not the data
+flow. Checked entrywise against the oracle over each rank's whole C block,
+and the pulled volume byte-exact.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, mL, nL, K, q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import helpers as H
+    from oracle import oracle as O
+    from paper_1904_05717_b200 import multigpu as MG
+    from paper_1904_05717_b200 import tilemul as T
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        lay = MG.make_layout(world, mL, nL, K)
+        rows, cols = MG.Summa.groups(dist, lay)
+        r, c = lay.coords(rank)
+        A = torch.empty(lay.mL * lay.K // lay.Pc, dtype=torch.float64, device=dev)
+        B = torch.empty(lay.K // lay.Pr * lay.nL, dtype=torch.float64, device=dev)
+        C = torch.empty(lay.mL * lay.nL, dtype=torch.float64, device=dev)
+        MG.fill_local(lay, rank, A, B, C, T.fill_uniform_block)
+        torch.cuda.synchronize()
+        C0 = C.cpu().numpy().copy()
+        hier = T.gpu_hierarchy(128)
+        d = T.parse_name("C2A1C0")
+        bs = T.derive_blocksizes(d, hier, T.Shape(lay.mL, lay.nL, lay.KC),
+                                 opts=T.DeriveOptions(micro=T.MicroTile(128, 128)),
+                                 pinned=T.BlocksizeSet({(1, "m"): 128}))
+        nest = T.build_plan(d, bs, hier, T.Shape(lay.mL, lay.nL, lay.KC))
+
+        def gemm(a, b, cc):
+            T.execute(nest, a, b, cc, T.ExecOptions())
+
+        s = MG.Summa(lay, rank, dev, gemm, dist, rows[r], cols[c])
+        s.attach_peers(A, B)
+        s.run(A, B, C)
+        torch.cuda.synchronize()
+        with pytest.raises(ValueError):  # per-step uploads need the broadcasts
+            s.run(A, B, C, ready=[None] * lay.chunks)
+        s.detach_peers()
+        got = C.cpu().numpy()
+        # reference: every entry of this rank's block from the global seeded matrices
+        gi = np.arange(lay.mL) + r * lay.mL
+        gj = np.arange(lay.nL) + c * lay.nL
+        p = np.arange(lay.K)
+        Ag = O.counter_uniform(11, (gi[:, None] + p[None, :] * lay.M).astype(np.uint64))
+        Bg = O.counter_uniform(12, (p[:, None] + gj[None, :] * lay.K).astype(np.uint64))
+        want = (C0.reshape(lay.nL, lay.mL).T + Ag @ Bg)
+        ab = np.abs(Ag) @ np.abs(Bg)
+        ok, worst = H.entrywise_ok(got.reshape(lay.nL, lay.mL).T.ravel(), want.ravel(), ab.ravel(), lay.K,
+                                   c0=C0.reshape(lay.nL, lay.mL).T.ravel())
+        expect = 8 * (lay.mL * lay.K * (lay.Pc - 1) // lay.Pc + lay.nL * lay.K * (lay.Pr - 1) // lay.Pr)
+        q.put((rank, ok, worst, s.exchanged_bytes, expect, None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # report instead of hanging the parent
+        import traceback
+
+        q.put((rank, False, float("nan"), 0, 0, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_copy_engine_exchange_matches_oracle(world):
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 256, 384, 1024, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, ok, worst, got_bytes, want_bytes, tb in res:
+        assert tb is None, tb
+        assert ok, (rank, worst)
+        assert got_bytes == want_bytes, (rank, got_bytes, want_bytes)
