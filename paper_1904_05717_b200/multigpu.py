@@ -304,7 +304,7 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
         T.execute(nest, a, b, cc, opts)
 
     s = Summa(lay, rank, dev, gemm, dist, rows[r], cols[c])
-    exchange = "nccl broadcasts"
+    exchange = "nccl broadcasts" if world > 1 else "none (one rank)"
     if world > 1 and os.environ.get("TILEMUL_EXCHANGE", "ce") == "ce":
         try:  # copy-engine pulls over peer memory; the broadcasts if the peers cannot be mapped
             s.attach_peers(A, B)
