@@ -204,7 +204,8 @@ class Summa:
                 self.exchanged_bytes += b.numel() * 8
         return a, b, works
 
-    def run(self, A_local, B_local, C_local, ready=None, comm=None) -> None:
+    def run(self, A_local, B_local, C_local, ready=None, comm=None, blocks=None, c_ready=None, gemm_block=None,
+            block_done=None) -> None:
         """C_local += A_r · B_c over all K chunks (ascending k).
 
         ready[j] (CUDA events, optional): this rank's own pieces of chunk j
@@ -212,12 +213,18 @@ class Summa:
         its exchange is then posted from `comm`, which waits for it and for
         the compute work issued so far (the receive buffer it overwrites was
         last read by the GEMM two chunks back), so uploads, exchanges and
-        GEMMs overlap."""
+        GEMMs overlap.
+
+        blocks [(col0, col1), ...] with gemm_block(a, b_cols, c_cols): the
+        first and last chunks run per column block of C, the first waiting
+        for c_ready[q] (that block of C uploaded), the last calling
+        block_done(q) once block q is final -- so C's upload and download
+        stream under the GEMMs instead of bracketing them."""
         L = self.lay.chunks
         if ready is not None and self.peer_a is not None:
             raise ValueError("copy-engine pulls read the peers' pieces in place: per-step uploads need the broadcasts")
         cur = None
-        if comm is not None:
+        if comm is not None or c_ready is not None:
             import torch
 
             cur = torch.cuda.current_stream()
@@ -242,7 +249,86 @@ class Summa:
                 cur.wait_event(ready[j])
             if j + 1 < L:
                 pending = post(j + 1)  # overlaps the GEMM below
-            self.gemm(a, b, C_local)
+            if blocks is None or 0 < j < L - 1:
+                self.gemm(a, b, C_local)
+                continue
+            lay = self.lay
+            for q, (j0, j1) in enumerate(blocks):
+                if j == 0 and c_ready is not None:
+                    cur.wait_event(c_ready[q])
+                gemm_block(a, b[j0 * lay.KC:j1 * lay.KC], C_local[j0 * lay.mL:j1 * lay.mL])
+                if j == L - 1 and block_done is not None:
+                    block_done(q)
+
+
+class HostStep:
+    """One e2e step of a rank: its pinned-host A/B pieces and C block in,
+    C += A_r·B_c, C back -- with the copies streamed under the GEMMs. On a
+    copy stream: C column block 0, this rank's chunk-0 pieces, the other C
+    blocks, then the later chunks' pieces; each chunk's exchange is posted once
+    its own pieces are up. The first chunk's GEMM runs block by block as C
+    arrives; the last one block by block, each block sent back to the host on
+    a third stream as soon as it is final."""
+
+    def __init__(self, summa: "Summa", A, B, C, plan_for_width: Callable, execute: Callable, max_blocks: int = 8):
+        import torch
+
+        lay = summa.lay
+        self.s, self.A, self.B, self.C = summa, A, B, C
+        dev = summa.device
+        nb = max(1, min(max_blocks, lay.nL // 1024))
+        wb = -(-lay.nL // nb)
+        self.blocks = [(q * wb, min(lay.nL, (q + 1) * wb)) for q in range(nb) if q * wb < lay.nL]
+        self.nests = {w: plan_for_width(w) for w in {j1 - j0 for j0, j1 in self.blocks}}
+        self.execute = execute
+        self.copy = torch.cuda.Stream(device=dev)
+        self.comm = torch.cuda.Stream(device=dev)
+        self.d2h = torch.cuda.Stream(device=dev)
+
+    def run(self, Ah, Bh, Ch) -> None:
+        import torch
+
+        s, lay, A, B, C = self.s, self.s.lay, self.A, self.B, self.C
+        compute = torch.cuda.current_stream(s.device)
+        sa, sb = lay.mL * lay.KC, lay.KC * lay.nL
+        ready, c_ready = [], []
+
+        def up_c(q):
+            j0, j1 = self.blocks[q]
+            C[j0 * lay.mL:j1 * lay.mL].copy_(Ch[j0 * lay.mL:j1 * lay.mL], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.copy)
+            c_ready.append(ev)
+
+        self.copy.wait_stream(compute)
+        with torch.cuda.stream(self.copy):
+            up_c(0)
+            for j in range(lay.chunks):
+                if lay.a_owner(j) == s.c:
+                    q = lay.a_local_chunk(j)
+                    A[q * sa:(q + 1) * sa].copy_(Ah[q * sa:(q + 1) * sa], non_blocking=True)
+                if lay.b_owner(j) == s.r:
+                    q = lay.b_local_chunk(j)
+                    B[q * sb:(q + 1) * sb].copy_(Bh[q * sb:(q + 1) * sb], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.copy)
+                ready.append(ev)
+                if j == 0:
+                    for q in range(1, len(self.blocks)):
+                        up_c(q)
+
+        def gemm_block(a, b, cc):
+            self.execute(self.nests[cc.numel() // lay.mL], a, b, cc)
+
+        def block_done(q):
+            j0, j1 = self.blocks[q]
+            self.d2h.wait_stream(compute)
+            with torch.cuda.stream(self.d2h):
+                Ch[j0 * lay.mL:j1 * lay.mL].copy_(C[j0 * lay.mL:j1 * lay.mL], non_blocking=True)
+
+        s.run(A, B, C, ready=ready, comm=self.comm, blocks=self.blocks, c_ready=c_ready, gemm_block=gemm_block,
+              block_done=block_done)
+        compute.wait_stream(self.d2h)
 
 
 class _StreamWait:
@@ -340,32 +426,11 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
     if not args.no_e2e:
         Ah, Bh, Ch = (x.cpu().pin_memory() for x in (A, B, C))
         steps = max(1, min(args.steps, 3))
-        copy = torch.cuda.Stream(device=dev)
-        comm = torch.cuda.Stream(device=dev)
-        compute = torch.cuda.current_stream(dev)
-        sa, sb = lay.mL * lay.KC, lay.KC * lay.nL
+        hs = HostStep(s, A, B, C, lambda w: make_plan(T, lay.mL, w, lay.KC)[0],
+                      lambda nest, a, b, cc: T.execute(nest, a, b, cc, opts))
 
         def one_step():
-            # C first; then this rank's A/B chunk pieces in chunk order on a copy
-            # stream, each chunk's exchange posted only once its own pieces are up
-            ready = {}
-            copy.wait_stream(compute)
-            with torch.cuda.stream(copy):
-                C.copy_(Ch, non_blocking=True)
-                ev_c = torch.cuda.Event()
-                ev_c.record(copy)
-                for j in range(lay.chunks):
-                    if lay.a_owner(j) == c:
-                        q = lay.a_local_chunk(j)
-                        A[q * sa:(q + 1) * sa].copy_(Ah[q * sa:(q + 1) * sa], non_blocking=True)
-                    if lay.b_owner(j) == r:
-                        q = lay.b_local_chunk(j)
-                        B[q * sb:(q + 1) * sb].copy_(Bh[q * sb:(q + 1) * sb], non_blocking=True)
-                    ready[j] = torch.cuda.Event()
-                    ready[j].record(copy)
-            compute.wait_event(ev_c)
-            s.run(A, B, C, ready=[ready[j] for j in range(lay.chunks)], comm=comm)
-            Ch.copy_(C, non_blocking=True)
+            hs.run(Ah, Bh, Ch)
 
         torch.cuda.synchronize()
         dist.barrier()
@@ -381,8 +446,9 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
         e2e = {"value": 2.0 * lay.M * lay.N * lay.K / te / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": 8 * (A.numel() + B.numel() + C.numel()) * world,
                "d2h_bytes_per_step": 8 * C.numel() * world, "ms_per_step": te * 1e3,
-               "path": "per rank: pinned host C block up, then its A/B chunk pieces streamed under the 2-D "
-                       "partitioned GEMM (each chunk's exchange waits for its upload), C block back"}
+               "path": "per rank: pinned host C in column blocks and its A/B chunk pieces streamed under the 2-D "
+                       "partitioned GEMM (first chunk per C block as it arrives, each chunk's exchange after its "
+                       "upload), each C block sent back as soon as the last chunk has finished it"}
     peak = T.measure_fp64_peak(10)
     if rank == 0:
         print(json.dumps({

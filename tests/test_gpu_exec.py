@@ -305,6 +305,57 @@ def test_multigpu_driver_world1_nccl():
         dist.destroy_process_group()
 
 
+def test_multigpu_host_step_world1_nccl():
+    """The driver's e2e step (multigpu.HostStep): pinned-host pieces in, C in
+    column blocks streamed under the first chunk's GEMM and sent back block by
+    block after the last one; the device buffers start zeroed, so every input
+    must arrive through the pipeline, and the host C must hold the product."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1904_05717_b200 import multigpu as MG
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        lay = MG.make_layout(1, 384, 2560, 2048)  # 2 chunks, 2 C blocks of 1280 columns
+        A = torch.empty(lay.mL * lay.K, dtype=torch.float64, device="cuda")
+        B = torch.empty(lay.K * lay.nL, dtype=torch.float64, device="cuda")
+        Cd = torch.empty(lay.mL * lay.nL, dtype=torch.float64, device="cuda")
+        MG.fill_local(lay, 0, A, B, Cd, T.fill_uniform_block)
+        Ah, Bh, Ch = (x.cpu().pin_memory() for x in (A, B, Cd))
+        c0 = Ch.numpy().copy()
+        for x in (A, B, Cd):
+            x.zero_()
+        import bench
+
+        nest, _, _ = bench.make_plan(T, lay.mL, lay.nL, lay.KC)
+        rows, cols = MG.Summa.groups(dist, lay)
+        sm = MG.Summa(lay, 0, torch.device("cuda"), lambda a, b, c: T.execute(nest, a, b, c), dist, rows[0], cols[0])
+        hs = MG.HostStep(sm, A, B, Cd, lambda w: bench.make_plan(T, lay.mL, w, lay.KC)[0],
+                         lambda n, a, b, c: T.execute(n, a, b, c))
+        assert len(hs.blocks) == 2
+        hs.run(Ah, Bh, Ch)
+        torch.cuda.synchronize()
+        got = Ch.numpy()
+        rng = np.random.default_rng(2)
+        ii, jj = rng.integers(0, lay.mL, 512), rng.integers(0, lay.nL, 512)
+        p = np.arange(lay.K)
+        a_rows = O.counter_uniform(11, (ii[:, None] + p[None, :] * lay.M).astype(np.uint64))
+        b_cols = O.counter_uniform(12, (p[None, :] + jj[:, None] * lay.K).astype(np.uint64))
+        want = c0[ii + jj * lay.mL] + np.einsum("tp,tp->t", a_rows, b_cols)
+        ab = np.einsum("tp,tp->t", np.abs(a_rows), np.abs(b_cols))
+        ok, worst = H.entrywise_ok(got[ii + jj * lay.mL], want, ab, lay.K, c0=c0[ii + jj * lay.mL])
+        assert ok, worst
+    finally:
+        dist.destroy_process_group()
+
+
 @pytest.mark.parametrize("split", [0, 3, -1])
 def test_split_k_tail_and_uniform(split):
     """split_k=-1 (stream-K: equal contiguous (tile, k-slab) ranges per CTA),
