@@ -31,6 +31,9 @@ namespace mmm {
 namespace gpu {
 namespace {
 
+#ifndef TC_CPF_AHEAD
+#define TC_CPF_AHEAD 8  // k-blocks before the end of a tile at which the pair kernel prefetches its C
+#endif
 constexpr int kTcStages = 4;
 constexpr int kTcBM = 128, kTcBN = 256;
 
@@ -54,6 +57,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "bra TC_WAIT;\n"
         "TC_DONE:\n\t}\n" ::"r"(saddr(b)),
         "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_cta(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(saddr(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -137,6 +152,8 @@ struct TcArgs {
     int64_t ldc;
     const Task* tasks;
     int32_t ntasks;
+    int64_t m = 0, n = 0;   // C extents (the TMA epilogue's clipping bounds)
+    int32_t tma_c = 0;      // 256 x 512 pair kernel: tmC maps C (16-byte aligned columns) for the TMA epilogue
 };
 
 template <bool TF32>
@@ -471,7 +488,8 @@ __host__ __device__ constexpr uint32_t instr_desc_pair() {
 
 template <bool TF32, int NH = 1>
 __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __grid_constant__ CUtensorMap tmA,
-                                                                  const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+                                                                  const __grid_constant__ CUtensorMap tmB, TcArgs a,
+                                                                  const __grid_constant__ CUtensorMap tmC) {
     using G = Tc2Geo<TF32, NH>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -479,7 +497,8 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
     uint64_t* empty = full + G::STAGES;
     uint64_t* tfull = empty + G::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* cl = tempty + 2;  // TMA epilogue: C quarter loads into the (then idle) stage ring, 3 buffers
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cl + 3);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -499,6 +518,7 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], 2 * G::EPI_WARPS);
         }
+        for (int s = 0; s < 3; ++s) mbar_init(&cl[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 2) {
@@ -520,6 +540,14 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
                 const int nk = (t.k + G::BK - 1) / G::BK;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
+                    if (NH == 2 && a.tma_c && kb == nk - TC_CPF_AHEAD) {
+                        // the TMA epilogue reads this CTA's C quarters right after the k loop: warm L2 with them
+                        for (int q = 0; q < 4; ++q)
+                            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                                             reinterpret_cast<uint64_t>(&tmC)),
+                                         "r"(t.i0 + static_cast<int>(rank) * 128), "r"(t.j0 + q * 128)
+                                         : "memory");
+                    }
                     uint8_t* sa = smem + stage * G::STAGE;
                     uint8_t* sb = sa + G::A_BYTES;
                     if (leader) mbar_expect_tx(&full[stage], G::PAIR_STAGE_BYTES);
@@ -585,10 +613,68 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
         const int row = static_cast<int>(rank) * 128 + ew * 32 + lane;
         int acc = 0;
         uint32_t aphase = 0;
-        for (int ti = cluster; ti < a.ntasks; ti += nclusters) {
+        uint32_t ntask = 0;
+        for (int ti = cluster; ti < a.ntasks; ti += nclusters, ++ntask) {
             const Task t = a.tasks[ti];
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
+            // TMA epilogue (256 x 512 pair tiles, one task per cluster so the stage ring is idle): C moves
+            // between L2 and shared memory in 128-row x 128-column quarters by bulk tensor copies, three
+            // buffers in the ring, and each lane adds its TMEM row into shared memory. A box store writes
+            // its whole box, clipped only at C's edges, so the task must cover its box region.
+            if constexpr (NH == 2) {
+                const bool covers = (t.m == 256 || static_cast<int64_t>(t.i0) + t.m == a.m) &&
+                                    (t.n == 512 || static_cast<int64_t>(t.j0) + t.n == a.n);
+                if (a.tma_c && covers && a.ntasks <= nclusters) {
+                    constexpr uint32_t QB = 128 * 128 * 4;  // bytes of one quarter
+                    const uint32_t cbase = saddr(smem);
+                    const int r0 = t.i0 + static_cast<int>(rank) * 128;
+                    const bool issuer = warp == 4 && lane == 0;
+                    const uint32_t ph = ntask & 1;  // cl[1], cl[2] complete once per task, cl[0] twice
+                    if (issuer) {
+                        for (int q = 0; q < 3; ++q) {
+                            mbar_expect_tx(&cl[q], QB);
+                            tma_load_2d_cta(cbase + q * QB, &tmC, &cl[q], r0, t.j0 + q * 128);
+                        }
+                    }
+                    const int g = (warp - 4) >> 2;  // this warp's 64 columns of each quarter
+                    for (int q = 0; q < 4; ++q) {
+                        const int buf = q % 3;
+                        mbar_wait(&cl[buf], buf == 0 ? (q == 0 ? 0u : 1u) : ph);
+                        float* cs = reinterpret_cast<float*>(smem + buf * QB);
+#pragma unroll 1
+                        for (int cc = 0; cc < 2; ++cc) {
+                            const int col = g * 64 + cc * 32;
+                            uint32_t r[32];
+                            TC_LD32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) +
+                                        static_cast<uint32_t>(q * 128 + col), r);
+                            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) cs[(col + j) * 128 + ew * 32 + lane] += __uint_as_float(r[j]);
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * G::EPI_WARPS) : "memory");
+                        if (issuer) {
+                            tma_store_2d(&tmC, cbase + buf * QB, r0, t.j0 + q * 128);
+                            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                            if (q == 0) {  // quarter 3 reuses buffer 0 once the store has read it
+                                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                                mbar_expect_tx(&cl[0], QB);
+                                tma_load_2d_cta(cbase, &tmC, &cl[0], r0, t.j0 + 3 * 128);
+                            }
+                        }
+                    }
+                    if (issuer) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(mapa_rank(&tempty[acc], 0));
+                    if (++acc == G::NACC) {
+                        acc = 0;
+                        aphase ^= 1;
+                    }
+                    continue;
+                }
+            }
             const bool live = row < t.m;
             float* crow = a.C + (static_cast<int64_t>(t.i0) + row) + static_cast<int64_t>(t.j0 + h * 256) * a.ldc;
 #pragma unroll 1
@@ -723,6 +809,20 @@ cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb,
         attr[TF32] = true;
     }
     TcArgs args{C, ldc, tasks, ntasks};
+    args.m = m;
+    args.n = n;
+    CUtensorMap mc;
+    std::memset(&mc, 0, sizeof(mc));
+    if (NH == 2 && (ldc * 4) % 16 == 0 && reinterpret_cast<uintptr_t>(C) % 16 == 0) {
+        // C quarters for the TMA epilogue: 128 rows x 128 columns of fp32, unswizzled ([col][128 rows])
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(m), static_cast<cuuint64_t>(n)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc) * 4};
+        const cuuint32_t box[2] = {128, 128}, estr[2] = {1, 1};
+        args.tma_c = g_encode(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        if (const char* env = std::getenv("TILEMUL_TC_TMA_EPILOGUE")) args.tma_c &= std::atoi(env);
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
     cfg.blockDim = dim3(G::THREADS);
@@ -735,7 +835,7 @@ cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb,
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_tc2<TF32, NH>, ma, mb, args);
+    return cudaLaunchKernelEx(&cfg, k_tc2<TF32, NH>, ma, mb, args, mc);
 }
 
 }  // namespace
