@@ -121,28 +121,48 @@ class Summa:
         cols = [dist.new_group([lay.rank_of(r, c) for r in range(lay.Pr)]) for c in range(lay.Pc)]
         return rows, cols
 
-    def attach_peers(self, A_local, B_local) -> None:
+    def attach_peers(self, A_local, B_local) -> bool:
         """Copy-engine exchange: map every row peer's A pieces and column
         peer's B pieces (CUDA IPC; all ranks must call, after filling their
-        pieces). The pieces must stay unchanged while peers read them."""
+        pieces). The pieces must stay unchanged while peers read them.
+        Collective and all-or-nothing: returns whether every rank mapped its
+        peers; if any could not, no rank pulls (the broadcasts stay in use)."""
         import torch
-        from torch.multiprocessing.reductions import reduce_tensor
 
         lay = self.lay
-        mine = (reduce_tensor(A_local), reduce_tensor(B_local))
+        mine, err = None, None
+        try:
+            from torch.multiprocessing.reductions import reduce_tensor
+
+            mine = (reduce_tensor(A_local), reduce_tensor(B_local))
+        except Exception as exc:  # noqa: BLE001 -- e.g. allocations IPC cannot export
+            err = exc
         allh = [None] * (lay.Pr * lay.Pc)
         self.dist.all_gather_object(allh, mine)
-        self.peer_a, self.peer_b = {}, {}
-        for c in range(lay.Pc):
-            if c != self.c:
-                fn, args = allh[lay.rank_of(self.r, c)][0]
-                self.peer_a[c] = fn(*args)
-        for r in range(lay.Pr):
-            if r != self.r:
-                fn, args = allh[lay.rank_of(r, self.c)][1]
-                self.peer_b[r] = fn(*args)
+        peer_a, peer_b = {}, {}
+        if err is None and all(h is not None for h in allh):
+            try:
+                for c in range(lay.Pc):
+                    if c != self.c:
+                        fn, args = allh[lay.rank_of(self.r, c)][0]
+                        peer_a[c] = fn(*args)
+                for r in range(lay.Pr):
+                    if r != self.r:
+                        fn, args = allh[lay.rank_of(r, self.c)][1]
+                        peer_b[r] = fn(*args)
+            except Exception as exc:  # noqa: BLE001
+                err = exc
+        else:
+            err = err or RuntimeError("a peer could not export its pieces")
+        ok = [err is None]
+        oks = [None] * (lay.Pr * lay.Pc)
+        self.dist.all_gather_object(oks, ok)  # every rank maps its peers before any rank relies on it
+        if not all(o[0] for o in oks):
+            self.peer_a = self.peer_b = None
+            return False
+        self.peer_a, self.peer_b = peer_a, peer_b
         self.ce_stream = torch.cuda.Stream(device=self.device)
-        self.dist.barrier()  # every rank holds its peers' mappings before any rank frees or reuses its pieces
+        return True
 
     def detach_peers(self) -> None:
         """Back to the broadcasts (collective: call on every rank)."""
@@ -392,13 +412,9 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
     s = Summa(lay, rank, dev, gemm, dist, rows[r], cols[c])
     exchange = "nccl broadcasts" if world > 1 else "none (one rank)"
     if world > 1 and os.environ.get("TILEMUL_EXCHANGE", "ce") == "ce":
-        try:  # copy-engine pulls over peer memory; the broadcasts if the peers cannot be mapped
-            s.attach_peers(A, B)
-            exchange = "copy-engine pulls over CUDA IPC peer mappings"
-        except Exception as exc:  # noqa: BLE001
-            exchange = f"nccl broadcasts (peer mapping failed: {type(exc).__name__})"
-            s.peer_a = s.peer_b = None
-            dist.barrier()
+        # copy-engine pulls over peer memory; the broadcasts (on every rank) if any rank cannot map its peers
+        exchange = ("copy-engine pulls over CUDA IPC peer mappings" if s.attach_peers(A, B)
+                    else "nccl broadcasts (peer mapping failed)")
     for _ in range(args.warmup):
         s.run(A, B, C)
     torch.cuda.synchronize()

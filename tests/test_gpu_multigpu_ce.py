@@ -68,7 +68,7 @@ def _worker(rank, world, port, mL, nL, K, q):
             T.execute(nest, a, b, cc, T.ExecOptions())
 
         s = MG.Summa(lay, rank, dev, gemm, dist, rows[r], cols[c])
-        s.attach_peers(A, B)
+        assert s.attach_peers(A, B)
         s.run(A, B, C)
         torch.cuda.synchronize()
         with pytest.raises(ValueError):  # per-step uploads need the broadcasts
