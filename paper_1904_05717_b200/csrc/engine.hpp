@@ -42,7 +42,7 @@ struct Schedule {
     int64_t work_ld = 0, work_slice = 0;
     int device = -1;
     int tma_ok = -1;         // task list fits the TMA kernel's slab grid (-1 = not yet checked)
-    int64_t max_task_k = 0;  // longest task k range (set with tma_ok)
+    int64_t slabs_per_cta = 0;  // k-slabs a CTA streams in one launch, on average (set with tma_ok)
     ~Schedule() {
         if (tasks) cudaFree(tasks);
         if (progress) cudaFree(progress);
@@ -84,7 +84,7 @@ int sm_count();
 // options allow and the operands/task list fit it, else the cp.async one.
 // Returns the staging used (TM_STAGING_*; 0 = kernel without variants).
 int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t K, bool vec16, int32_t staging,
-                 cudaStream_t stream);
+                 cudaStream_t stream, bool long_ok = false);
 // `tma`: the operands allow TMA staging (16-byte aligned bases and leading
 // dimensions, staging not forced to cp.async).
 gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o, bool tma);

@@ -437,31 +437,34 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
 }
 
 int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t K, bool vec16, int32_t staging,
-                 cudaStream_t stream) {
+                 cudaStream_t stream, bool long_ok) {
     if (staging < TM_STAGING_AUTO || staging > TM_STAGING_TMA) fail_usage("staging must be 0 (auto), 1 (cp.async) or 2 (TMA)");
     const int bk = gpu::tma_bk(s.kernel);
     if (staging == TM_STAGING_TMA && bk == 0) fail_usage("TMA staging exists for the DMMA kernels only");
     if (bk > 0 && s.tma_ok < 0) {
         s.tma_ok = 1;
-        s.max_task_k = 0;
+        int64_t slabs = 0;
         for (const auto& t : s.host_tasks) {
             if (t.k % bk != 0 && static_cast<int64_t>(t.p0) + t.k != K) s.tma_ok = 0;
-            s.max_task_k = std::max<int64_t>(s.max_task_k, t.k);
+            slabs += (t.k + bk - 1) / bk;
         }
+        s.slabs_per_cta = slabs / std::max(1, s.grid);
     }
-    // Auto takes TMA for the 128x128 kernel when no task is longer than
-    // kTmaAutoMaxK. Measured on one B200: TMA is 0.4-1.7
-    // points of FP64 peak faster than cp.async on every config, but its CTAs
-    // drift apart along long k ranges (the copies never stall them), so the
-    // wave stops sharing A/B panels in L2: HBM reads at 16384^3 grow 4-6x
-    // (1.6x / 2.2x at k = 4096 / 8192 with 16384^2 C, equal at 4096^3). A
-    // wave gate (CTAs of a round wait for the round's average k progress)
-    // restored the traffic but cost 2-4 points, more than TMA gains
-    // (profiles/tma_l2_r01.json). The 128x64 / 64x64 TMA variants trail
-    // cp.async by 0.5-4 points.
-    constexpr int64_t kTmaAutoMaxK = 4096;
+    // Auto takes TMA for the 128x128 kernel when a CTA streams at most
+    // kTmaAutoMaxSlabs k-slabs in the launch. Measured on one B200 (DESIGN.md
+    // 4.2): TMA is 0.4-1.7 points of FP64 peak faster than cp.async on every
+    // config, but its CTAs drift apart over a long launch (the copies never
+    // stall them), so the CTAs of a wave stop reading shared A/B panels
+    // within L2's reach. HBM reads over cp.async's grow with the launch's
+    // length in slabs per CTA: 1.2x at ~7k (8192^3, 1.32x the model), 1.6x at
+    // ~14k, 2.2x at ~28k, 5.5x at ~56k (16384^3). A wave gate (CTAs of a
+    // round wait for the round's average progress) restored the traffic but
+    // cost 2-4 points, more than TMA gains (profiles/tma_l2_r01.json). The
+    // 128x64 / 64x64 TMA variants trail cp.async by 0.5-4 points.
+    constexpr int64_t kTmaAutoMaxSlabs = 8192;
     const bool want = staging == TM_STAGING_TMA ||
-                      (staging == TM_STAGING_AUTO && s.kernel == gpu::kDmma128 && s.max_task_k <= kTmaAutoMaxK);
+                      (staging == TM_STAGING_AUTO && s.kernel == gpu::kDmma128 &&
+                       (long_ok || s.slabs_per_cta <= kTmaAutoMaxSlabs));
     if (bk > 0 && want) {
         // TMA boxes start on 16-byte boundaries of a column: the alignment the
         // 16-byte cp.async path needs too (even task origins, even ld, aligned bases)

@@ -219,12 +219,13 @@ def test_tma_config1_golden_entries():
     assert np.array_equal(got, ref)
 
 
-def test_tma_long_k_auto_stays_cpasync():
-    """Tasks longer than 4096 in k: auto stays on cp.async (TMA CTAs drift
-    apart along long k and lose the wave's L2 sharing, profiles/tma_l2_r01.json);
-    an explicit TMA launch is bitwise equal."""
-    m = n = 512
-    k = 8192 + 64
+def test_tma_long_launch_auto_stays_cpasync():
+    """A launch in which a CTA streams more than 8192 k-slabs: auto stays on
+    cp.async (TMA CTAs drift apart over long launches and lose the wave's L2
+    sharing, profiles/tma_l2_r01.json); an explicit TMA launch is bitwise
+    equal. One 128 x 128 tile, k = 8193 slabs + 16."""
+    m = n = 128
+    k = 32 * 8193 + 16
     nest = fused_nest(m, n, k)
     a, b, c = O.fill_uniform(77, [(m, k), (k, n), (m, n)])
     A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
@@ -233,8 +234,13 @@ def test_tma_long_k_auto_stays_cpasync():
     got, st = run(nest, A, B, c, split_k=1, staging="tma")
     assert st == "tma"
     assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
-    ii = np.arange(0, m, 7)
-    jj = (ii * 3) % n
+    ii = np.arange(0, m, 3)
+    jj = (ii * 5) % n
     want, ab = O.entries(k, a, m, b, k, c, m, ii, jj)
     ok, worst = H.entrywise_ok(got[ii + jj * m], want, ab, k, c0=c[ii + jj * m])
     assert ok, worst
+    # a short launch of the same kernel: auto takes TMA
+    nest2 = fused_nest(m, n, 4096)
+    a2, b2, c2 = O.fill_uniform(78, [(m, 4096), (4096, n), (m, n)])
+    _, st = run(nest2, torch.from_numpy(a2).cuda(), torch.from_numpy(b2).cuda(), c2, split_k=1)
+    assert st == "tma"
