@@ -176,7 +176,10 @@ int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, 
  * BASELINE configs[3]): C(m x n, fp32) += A·B with A, B column-major in BF16
  * (dtype TM_DTYPE_BF16) or in fp32 holding TF32 values (TM_DTYPE_TF32),
  * fp32 accumulation. Fused schedule only; bases and leading dimensions must
- * be 16-byte aligned (TMA). */
+ * be 16-byte aligned (TMA). opts->tile = 128: one SM per 128 x 256 tile;
+ * 0 / 256: SM pairs, 256 x 512 tiles (tile_n 0 / 512, the default) or
+ * 256 x 256 (tile_n = 256). Plan the nest with a register tile of the same
+ * shape so every task fills its tile. */
 enum { TM_DTYPE_BF16 = 1, TM_DTYPE_TF32 = 2 };
 int tm_execute_tc(tm_plan* plan, int dtype, const void* A, int64_t lda, const void* B, int64_t ldb, float* C,
                   int64_t ldc, const tm_exec_opts* opts, void* stream);
