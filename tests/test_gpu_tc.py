@@ -82,6 +82,40 @@ def test_tc_large_sampled(dtype, tile, tile_n):
     assert nest.last_launch()["tasks"] == (4096 // tile) * (4096 // (tile_n or (512 if tile == 256 else 256)))
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "tf32"])
+def test_tc_wide_tiles_partial_interior(dtype):
+    """256 x 512 pair tiles over a nest whose register blocks are 256 x 384:
+    interior tasks do not fill their tile's box, so they keep the per-lane
+    epilogue (a box store would overwrite the neighbouring task's C); the
+    edge tasks take the TMA epilogue. Full check against the oracle."""
+    m, n, k = 512, 1024, 200 if dtype == "tf32" else 208
+    hier = T.CacheHierarchy.from_capacities([256 * 512, 232448, 132644864 // 2])
+    d = T.parse_name("C2A1C0")
+    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(256, 384)),
+                             pinned=T.BlocksizeSet({(1, "m"): 256}))
+    nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+    assert nest.n_r == 384
+    A64 = torch.empty(m * k, dtype=torch.float64, device="cuda")
+    B64 = torch.empty(k * n, dtype=torch.float64, device="cuda")
+    T.fill_uniform_device(A64, 7)
+    T.fill_uniform_device(B64, 8)
+    A, B = T.round_inputs(A64, dtype), T.round_inputs(B64, dtype)
+    C0 = torch.empty(m * n, dtype=torch.float64, device="cuda")
+    T.fill_uniform_device(C0, 9)
+    C = C0.float()
+    c0 = C.double().cpu().numpy()
+    T.execute_tc(nest, A, B, C, dtype, T.ExecOptions(tile=256, tile_n=512))
+    torch.cuda.synchronize()
+    got = C.double().cpu().numpy()
+    a, b = A.double().cpu().numpy(), B.double().cpu().numpy()
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    ii, jj = ii.ravel(), jj.ravel()
+    want, ab = O.entries(k, a, m, b, k, c0, m, ii, jj)
+    idx = ii + jj * m
+    bound = (k + 2) * U32 * (ab + np.abs(c0[idx]))
+    assert np.all(np.abs(got[idx] - want) <= bound)
+
+
 def test_tc_rejects_unaligned_and_faithful():
     nest = tc_plan(130, 256, 64)  # lda = 130 bf16 = 260 bytes: not 16-byte aligned for TMA
     A = torch.zeros(130 * 64, dtype=torch.bfloat16, device="cuda")
