@@ -43,6 +43,8 @@ struct Schedule {
     int device = -1;
     int tma_ok = -1;         // task list fits the TMA kernel's slab grid (-1 = not yet checked)
     int64_t slabs_per_cta = 0;  // k-slabs a CTA streams in one launch, on average (set with tma_ok)
+    std::vector<int32_t> segments;  // TMA launches of a long task list: task index boundaries (whole rounds)
+    int last_launches = 1;          // task-kernel launches the last launch_tasks issued
     ~Schedule() {
         if (tasks) cudaFree(tasks);
         if (progress) cudaFree(progress);

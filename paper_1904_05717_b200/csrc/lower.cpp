@@ -461,7 +461,48 @@ int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t 
     // round wait for the round's average progress) restored the traffic but
     // cost 2-4 points, more than TMA gains (profiles/tma_l2_r01.json). The
     // 128x64 / 64x64 TMA variants trail cp.async by 0.5-4 points.
+    // A long strided task list is launched in segments of whole rounds (task
+    // r*G .. r*G+G-1 on CTA 0..G-1) of at most kTmaSegmentSlabs slabs per
+    // CTA: each kernel boundary brings the wave back in step. 16384^3 in 14
+    // segments of 4096 slabs: 54 GB of HBM reads per step (1.15x the model,
+    // cp.async's traffic; 69 GB with 8192-slab segments, 283 GB as one
+    // launch) at cp.async's 95.5 % of peak.
     constexpr int64_t kTmaAutoMaxSlabs = 8192;
+    static const int64_t kTmaSegmentSlabs = [] {  // (TILEMUL_TMA_SEGMENT_SLABS: A/B knob)
+        const char* env = std::getenv("TILEMUL_TMA_SEGMENT_SLABS");
+        return env ? std::max<int64_t>(1, std::atoll(env)) : int64_t{4096};
+    }();
+    s.last_launches = 1;
+    if (bk > 0 && staging == TM_STAGING_AUTO && s.kernel == gpu::kDmma128 && !long_ok && !s.blocked &&
+        s.slabs_per_cta > kTmaAutoMaxSlabs && s.tma_ok == 1 && vec16) {
+        if (s.segments.empty()) {
+            const std::size_t G = static_cast<std::size_t>(std::max(1, s.grid)), nt = s.host_tasks.size();
+            s.segments.push_back(0);
+            int64_t acc = 0;
+            for (std::size_t r0 = 0; r0 < nt; r0 += G) {
+                const int64_t round = (s.host_tasks[r0].k + bk - 1) / bk;
+                if (acc > 0 && acc + round > kTmaSegmentSlabs) {
+                    s.segments.push_back(static_cast<int32_t>(r0));
+                    acc = 0;
+                }
+                acc += round;
+            }
+            s.segments.push_back(static_cast<int32_t>(nt));
+        }
+        bool ok = true;
+        for (std::size_t q = 0; q + 1 < s.segments.size() && ok; ++q) {
+            gpu::Args sa = a;
+            sa.tasks = a.tasks + s.segments[q];
+            sa.ntasks = s.segments[q + 1] - s.segments[q];
+            const cudaError_t r = gpu::launch_tma(s.kernel, sa, M, N, K, std::min(s.grid, sa.ntasks), stream);
+            if (r == cudaErrorNotSupported && q == 0) ok = false;  // (decided before any launch)
+            else cuda_check(r, "task kernel launch (TMA segment)");
+        }
+        if (ok) {
+            s.last_launches = static_cast<int>(s.segments.size()) - 1;
+            return TM_STAGING_TMA;
+        }
+    }
     const bool want = staging == TM_STAGING_TMA ||
                       (staging == TM_STAGING_AUTO && s.kernel == gpu::kDmma128 &&
                        (long_ok || s.slabs_per_cta <= kTmaAutoMaxSlabs));
@@ -514,7 +555,7 @@ void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t l
     gpu::Args a{A, lda, B, ldb, C, ldc, s.tasks, static_cast<int32_t>(s.host_tasks.size()), s.progress, s.work,
                 s.work_ld, s.work_slice, s.blocked ? s.cta_first : nullptr};
     plan->last_staging = launch_tasks(s, a, e.m, e.n, e.k, vec16, o.staging, stream);
-    int launches = 1;
+    int launches = s.last_launches;
     if (s.slices > 0) {
         cuda_check(gpu::launch_reduce_tiles(C, ldc, s.work, s.work_ld, s.work_slice, s.reduce, s.slices, stream),
                    "split-k reduce launch");
