@@ -263,8 +263,10 @@ def our_arm(args):
     torch.cuda.synchronize()
     launches_per_step = nest.last_launch()["launches"]
     staging = nest.last_launch()["staging"]
-    kernel_name = ("k_dmma_tma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3> (16 warps, TMA 128B-swizzled slabs)"
-                   if staging == "tma" else "k_dmma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3,vec16> (16 warps, cp.async)")
+    kernel_name = ("k_dmma_tma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3> (16 warps, TMA 128B-swizzled slabs"
+                   + (f"; {launches_per_step} launches per step, segments of whole rounds" if launches_per_step > 1 else "")
+                   + ")" if staging == "tma" else
+                   "k_dmma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3,vec16> (16 warps, cp.async)")
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
@@ -340,7 +342,8 @@ def our_arm(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "FP64 DMMA issue-rate probe run live in this bench (MEASURED_PEAKS.json has no "
                                     "FP64 figure); nominal 148 SM x 64 FMA/clk x 1.965 GHz = 37.2",
-                     "kernel": kernel_name, "algorithmic_flops_per_launch": flops,
+                     "kernel": kernel_name, "algorithmic_flops_per_launch": flops / launches_per_step,
+                     "algorithmic_flops_per_step": flops, "launches_per_step": launches_per_step,
                      "traffic_source": traffic_src},
         "model": {"hbm_bytes_model": hbm_model_bytes,
                   "hbm_bytes_measured": traffic,

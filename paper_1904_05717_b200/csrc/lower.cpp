@@ -478,7 +478,7 @@ int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t 
         if (s.segments.empty()) {
             const std::size_t G = static_cast<std::size_t>(std::max(1, s.grid)), nt = s.host_tasks.size();
             s.segments.push_back(0);
-            int64_t acc = 0;
+            int64_t acc = 0, longest = 0;
             for (std::size_t r0 = 0; r0 < nt; r0 += G) {
                 const int64_t round = (s.host_tasks[r0].k + bk - 1) / bk;
                 if (acc > 0 && acc + round > kTmaSegmentSlabs) {
@@ -486,10 +486,13 @@ int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t 
                     acc = 0;
                 }
                 acc += round;
+                longest = std::max(longest, acc);
             }
             s.segments.push_back(static_cast<int32_t>(nt));
+            // rounds too long to cut (one task of > kTmaAutoMaxSlabs slabs per CTA): cp.async
+            if (longest > kTmaAutoMaxSlabs) s.segments.assign({-1});
         }
-        bool ok = true;
+        bool ok = s.segments.front() == 0;
         for (std::size_t q = 0; q + 1 < s.segments.size() && ok; ++q) {
             gpu::Args sa = a;
             sa.tasks = a.tasks + s.segments[q];
