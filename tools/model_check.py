@@ -37,7 +37,20 @@ def main():
         per.setdefault(int(r[ki]), {})[r[ni]] = v * mult
     launches = [per[k] for k in sorted(per)]
     if len(launches) != len(recs):
-        raise SystemExit(f"{len(launches)} profiled launches vs {len(recs)} cases")
+        # a case may be several task-kernel launches (TMA segments): group them by the case's launch count
+        want = sum(int(r.get("launch", {}).get("launches", 1)) for r in recs)
+        if want != len(launches):
+            raise SystemExit(f"{len(launches)} profiled launches vs {len(recs)} cases ({want} launches)")
+        grouped, at = [], 0
+        for r in recs:
+            nl = int(r.get("launch", {}).get("launches", 1))
+            g = {}
+            for m in launches[at:at + nl]:
+                for key, v in m.items():
+                    g[key] = g.get(key, 0.0) + v
+            grouped.append(g)
+            at += nl
+        launches = grouped
     out = []
     for rec, m in zip(recs, launches):
         dram = m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]
