@@ -450,8 +450,9 @@ int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t 
         }
         s.slabs_per_cta = slabs / std::max(1, s.grid);
     }
-    // Auto takes TMA for the 128x128 kernel when a CTA streams at most
-    // kTmaAutoMaxSlabs k-slabs in the launch. Measured on one B200 (DESIGN.md
+    // Auto takes TMA for the 128x128 kernel in launches in which a CTA
+    // streams at most kTmaAutoMaxSlabs k-slabs (longer task lists: segments,
+    // below). Measured on one B200 (DESIGN.md
     // 4.2): TMA is 0.4-1.7 points of FP64 peak faster than cp.async on every
     // config, but its CTAs drift apart over a long launch (the copies never
     // stall them), so the CTAs of a wave stop reading shared A/B panels
@@ -467,7 +468,7 @@ int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t 
     // segments of 4096 slabs: 54 GB of HBM reads per step (1.15x the model,
     // cp.async's traffic; 69 GB with 8192-slab segments, 283 GB as one
     // launch) at cp.async's 95.5 % of peak.
-    constexpr int64_t kTmaAutoMaxSlabs = 8192;
+    constexpr int64_t kTmaAutoMaxSlabs = 4096;
     static const int64_t kTmaSegmentSlabs = [] {  // (TILEMUL_TMA_SEGMENT_SLABS: A/B knob)
         const char* env = std::getenv("TILEMUL_TMA_SEGMENT_SLABS");
         return env ? std::max<int64_t>(1, std::atoll(env)) : int64_t{4096};
