@@ -106,11 +106,11 @@ cudaError_t kernel_info(Kernel kernel, KernelInfo* info);
 // (deterministic split-k reduction).
 cudaError_t launch_reduce_tiles(double* C, int64_t ldc, const double* work, int64_t work_ld, int64_t work_slice,
                                 const ReduceTile* tiles, int ntiles, cudaStream_t stream);
-// Sustained FP64 DMMA rate of this device (TFLOP/s) over `launches` probe launches.
 // Peak tcgen05 MMA rate of the current device (M=128 x N=256, BF16 or TF32
 // inputs, fp32 accumulate), best of `launches` launches of ~5 ms (burst) or
 // ~200 ms (sustained, power-capped), TFLOP/s.
 cudaError_t measure_tc_peak(bool tf32, int launches, bool sustained, double* tflops);
+// Sustained FP64 DMMA rate of this device (TFLOP/s) over `launches` probe launches.
 cudaError_t measure_fp64_peak(int launches, double* tflops);
 // tcgen05 BF16/TF32-input GEMM over a task list (C fp32, column-major).
 cudaError_t launch_tc(bool tf32, const void* A, int64_t lda, const void* B, int64_t ldb, float* C, int64_t ldc,

@@ -24,8 +24,9 @@ copied peer -> local receive buffer by the DMA engines on a side stream while
 chunk j's GEMM runs. NCCL's broadcast kernels need SMs, which the local
 GEMM's persistent grid holds entirely, so they can only run between GEMMs;
 the copy engines need none. The pieces a rank maps must not change while
-peers read them (the device-resident bench path; the e2e path, which uploads
-per step, keeps the broadcasts). The local GEMM is `tilemul.execute` on the
+peers read them: in the device-resident bench path they never change; the
+e2e path, which uploads them every step, orders uploads and pulls with
+cross-process CUDA events (Summa.attach_step_sync). The local GEMM is `tilemul.execute` on the
 sm_100a task kernel. The `gemm` hook exists so the CPU tests can drive the
 same schedule with a host matmul — the product path always passes the
 native GEMM.
@@ -107,6 +108,7 @@ class Summa:
         self.row_group, self.col_group = row_group, col_group
         self.peer_a = self.peer_b = None  # exchange="ce": peers' A pieces by column, B pieces by row
         self.ce_stream = None
+        self.step_sync = False  # attach_step_sync: pulls of pieces re-uploaded every step
         # receive buffers only where chunks actually arrive from peers
         self.abuf = [torch.empty(lay.mL * lay.KC, dtype=torch.float64, device=device)
                      for _ in range(2 if lay.Pc > 1 else 0)]
@@ -164,10 +166,87 @@ class Summa:
         self.ce_stream = torch.cuda.Stream(device=self.device)
         return True
 
+    def attach_step_sync(self) -> bool:
+        """Pulls for pieces that change every step (the e2e step re-uploads
+        them from the host). Collective, after attach_peers succeeded;
+        all-or-nothing like it. Per chunk, cross-process CUDA events (IPC):
+          up   -- recorded by the owner once its piece of chunk j is uploaded;
+                  a puller's copy of chunk j waits for it;
+          got  -- recorded by a puller once it has copied chunk j; the owner's
+                  next upload of that piece waits for it.
+        A stream waits on the last record issued before the wait, so two
+        host barriers per step (a gloo group: host-only, no SMs) order the
+        records and waits: step_begin before the uploads, step_published
+        between the uploads and the pulls. Only streams wait; no kernel
+        spins on another rank."""
+        import torch
+
+        lay = self.lay
+        err, mine = None, None
+        try:
+            self.ctrl = self.dist.new_group(backend="gloo")
+            ev = lambda: torch.cuda.Event(interprocess=True)  # noqa: E731
+            self.up_a = {j: ev() for j in range(lay.chunks) if lay.a_owner(j) == self.c}
+            self.up_b = {j: ev() for j in range(lay.chunks) if lay.b_owner(j) == self.r}
+            self.got = {j: ev() for j in range(lay.chunks)
+                        if lay.a_owner(j) != self.c or lay.b_owner(j) != self.r}
+            with torch.cuda.device(self.device):
+                mine = {k: {j: e.ipc_handle() for j, e in d.items()}
+                        for k, d in (("up_a", self.up_a), ("up_b", self.up_b), ("got", self.got))}
+        except Exception as exc:  # noqa: BLE001
+            err = exc
+        allh = [None] * (lay.Pr * lay.Pc)
+        self.dist.all_gather_object(allh, mine)
+        if err is None and all(h is not None for h in allh):
+            try:
+                open_ = lambda h: torch.cuda.Event.from_ipc_handle(self.device, h)  # noqa: E731
+                self.peer_up_a = {j: open_(allh[lay.rank_of(self.r, lay.a_owner(j))]["up_a"][j])
+                                  for j in range(lay.chunks) if lay.a_owner(j) != self.c}
+                self.peer_up_b = {j: open_(allh[lay.rank_of(lay.b_owner(j), self.c)]["up_b"][j])
+                                  for j in range(lay.chunks) if lay.b_owner(j) != self.r}
+                # pullers of my pieces: row peers for A chunk j, column peers for B chunk j
+                self.pullers = {j: [] for j in range(lay.chunks)}
+                for j in self.up_a:
+                    self.pullers[j] += [open_(allh[lay.rank_of(self.r, c)]["got"][j])
+                                        for c in range(lay.Pc) if c != self.c]
+                for j in self.up_b:
+                    self.pullers[j] += [open_(allh[lay.rank_of(r, self.c)]["got"][j])
+                                        for r in range(lay.Pr) if r != self.r]
+            except Exception as exc:  # noqa: BLE001
+                err = exc
+        else:
+            err = err or RuntimeError("a peer could not create its step events")
+        oks = [None] * (lay.Pr * lay.Pc)
+        self.dist.all_gather_object(oks, err is None)
+        self.step_sync = all(oks)
+        return self.step_sync
+
+    def step_begin(self) -> None:
+        """e2e step with pulls, before this rank issues its uploads: every
+        peer has issued its pulls of the previous step (their got records)."""
+        self.dist.barrier(group=self.ctrl)
+
+    def before_upload(self, stream, j: int) -> None:
+        """`stream` (the upload stream) waits until every peer has pulled this
+        rank's piece of chunk j in the previous step."""
+        for e in self.pullers[j]:
+            stream.wait_event(e)
+
+    def after_upload(self, stream, j: int) -> None:
+        if j in self.up_a:
+            self.up_a[j].record(stream)
+        if j in self.up_b:
+            self.up_b[j].record(stream)
+
+    def step_published(self) -> None:
+        """Every rank has issued this step's uploads (their up records)."""
+        self.dist.barrier(group=self.ctrl)
+
     def detach_peers(self) -> None:
         """Back to the broadcasts (collective: call on every rank)."""
         self.dist.barrier()  # no rank still pulls from a peer whose pieces are about to change
         self.peer_a = self.peer_b = None
+        self.step_sync = False
 
     def a_chunk_view(self, A_local, j: int):
         lay = self.lay
@@ -194,11 +273,17 @@ class Summa:
         st.wait_stream(torch.cuda.current_stream(self.device))  # the buffer's last reader (GEMM j-2) is queued there
         with torch.cuda.stream(st):
             if a_src_c != self.c:
+                if self.step_sync:
+                    st.wait_event(self.peer_up_a[j])
                 a.copy_(self.a_chunk_view(self.peer_a[a_src_c], j), non_blocking=True)
                 self.exchanged_bytes += a.numel() * 8
             if b_src_r != self.r:
+                if self.step_sync:
+                    st.wait_event(self.peer_up_b[j])
                 b.copy_(self.b_chunk_view(self.peer_b[b_src_r], j), non_blocking=True)
                 self.exchanged_bytes += b.numel() * 8
+            if self.step_sync:
+                self.got[j].record(st)
             ev = torch.cuda.Event()
             ev.record(st)
         return a, b, [_StreamWait(ev, self.device)]
@@ -241,8 +326,9 @@ class Summa:
         block_done(q) once block q is final -- so C's upload and download
         stream under the GEMMs instead of bracketing them."""
         L = self.lay.chunks
-        if ready is not None and self.peer_a is not None:
-            raise ValueError("copy-engine pulls read the peers' pieces in place: per-step uploads need the broadcasts")
+        if ready is not None and self.peer_a is not None and not self.step_sync:
+            raise ValueError("copy-engine pulls read the peers' pieces in place: per-step uploads need "
+                             "attach_step_sync (or the broadcasts)")
         cur = None
         if comm is not None or c_ready is not None:
             import torch
@@ -288,7 +374,9 @@ class HostStep:
     blocks, then the later chunks' pieces; each chunk's exchange is posted once
     its own pieces are up. The first chunk's GEMM runs block by block as C
     arrives; the last one block by block, each block sent back to the host on
-    a third stream as soon as it is final."""
+    a third stream as soon as it is final. With copy-engine pulls
+    (Summa.attach_step_sync) a peer's pull of chunk j waits for the owner's
+    upload of it, and the owner's next upload for its peers' pulls."""
 
     def __init__(self, summa: "Summa", A, B, C, plan_for_width: Callable, execute: Callable, max_blocks: int = 8):
         import torch
@@ -320,22 +408,31 @@ class HostStep:
             ev.record(self.copy)
             c_ready.append(ev)
 
+        pulls = s.peer_a is not None
+        if pulls:
+            s.step_begin()
         self.copy.wait_stream(compute)
         with torch.cuda.stream(self.copy):
             up_c(0)
             for j in range(lay.chunks):
+                if pulls:
+                    s.before_upload(self.copy, j)
                 if lay.a_owner(j) == s.c:
                     q = lay.a_local_chunk(j)
                     A[q * sa:(q + 1) * sa].copy_(Ah[q * sa:(q + 1) * sa], non_blocking=True)
                 if lay.b_owner(j) == s.r:
                     q = lay.b_local_chunk(j)
                     B[q * sb:(q + 1) * sb].copy_(Bh[q * sb:(q + 1) * sb], non_blocking=True)
+                if pulls:
+                    s.after_upload(self.copy, j)
                 ev = torch.cuda.Event()
                 ev.record(self.copy)
                 ready.append(ev)
                 if j == 0:
                     for q in range(1, len(self.blocks)):
                         up_c(q)
+        if pulls:
+            s.step_published()
 
         def gemm_block(a, b, cc):
             self.execute(self.nests[cc.numel() // lay.mL], a, b, cc)
@@ -437,8 +534,13 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
     per_gpu = flops / world / t / 1e12
 
     e2e = None
-    if s.peer_a is not None:
-        s.detach_peers()  # the e2e step re-uploads the pieces every step: broadcasts
+    e2e_exchange = exchange
+    if s.peer_a is not None and not args.no_e2e:
+        if s.attach_step_sync():
+            e2e_exchange = exchange + ", uploads and pulls ordered by cross-process CUDA events"
+        else:
+            s.detach_peers()  # no cross-process events: the e2e step exchanges with the broadcasts
+            e2e_exchange = "nccl broadcasts (step events unavailable)"
     if not args.no_e2e:
         Ah, Bh, Ch = (x.cpu().pin_memory() for x in (A, B, C))
         steps = max(1, min(args.steps, 3))
@@ -464,7 +566,8 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
                "d2h_bytes_per_step": 8 * C.numel() * world, "ms_per_step": te * 1e3,
                "path": "per rank: pinned host C in column blocks and its A/B chunk pieces streamed under the 2-D "
                        "partitioned GEMM (first chunk per C block as it arrives, each chunk's exchange after its "
-                       "upload), each C block sent back as soon as the last chunk has finished it"}
+                       "upload), each C block sent back as soon as the last chunk has finished it",
+               "exchange": e2e_exchange}
     peak = T.measure_fp64_peak(10)
     if rank == 0:
         print(json.dumps({
