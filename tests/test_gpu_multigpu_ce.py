@@ -193,3 +193,61 @@ def test_copy_engine_exchange_matches_oracle(world):
     if not torch.cuda.is_available():
         pytest.fail("CUDA device required for -m gpu tests")
     _spawn(_worker, world, 256, 384, 1024)
+
+
+def _bench_worker(rank, world, port, size, q):
+    """bench.py's N > 1 arm (multigpu.bench) end to end, gloo in place of
+    NCCL: the resident loop with copy-engine pulls, then the e2e steps with
+    the step events; rank 0's JSON line comes back through the queue."""
+    import argparse
+    import contextlib
+    import io
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    from paper_1904_05717_b200 import multigpu as MG
+    from paper_1904_05717_b200 import tilemul as T
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        args = argparse.Namespace(size=size, steps=2, warmup=3, no_e2e=False)
+        out = io.StringIO()
+        with contextlib.redirect_stdout(out):
+            rc = MG.bench(args, T, bench.make_plan, world, rank, 0)
+        q.put((rank, rc, out.getvalue(), None))
+    except Exception:  # report instead of hanging the parent
+        import traceback
+
+        q.put((rank, 1, "", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multigpu_bench_arm_world_gt1(world):
+    """The JSON line of the N > 1 bench arm: pulls in both the resident and
+    the e2e step, per-rank work = one size^2 C block (weak scaling)."""
+    import json
+
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, 1024, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    for rank, rc, _, tb in res:
+        assert tb is None, tb
+        assert rc == 0, rank
+    line = json.loads(res[0][2].strip().splitlines()[-1])
+    assert line["n_gpus"] == world and line["scaling"] == "weak" and line["value"] > 0
+    assert line["config"]["exchange"].startswith("copy-engine pulls")
+    assert line["e2e"]["exchange"].startswith("copy-engine pulls") and "events" in line["e2e"]["exchange"]
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
+    assert line["gpu_launches"] > 0 and line["exchanged_bytes_per_step_rank0"] > 0
