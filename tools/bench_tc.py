@@ -111,6 +111,29 @@ def main():
             print(json.dumps({"config": "config4", "impl": "cuBLAS (torch.matmul) reference", "dtype": dtype,
                               "shape": [m, n, k], "seconds": t, "tflops": 2.0 * m * n * k / t / 1e12,
                               "output": "bf16" if dtype == "bf16" else "fp32", "clocks": clk.summary()}), flush=True)
+            if dtype == "bf16":
+                # the same contract as ours: fp32 C += A·B from bf16 inputs (beta = 1, fp32 out)
+                C32 = torch.zeros(m, n, dtype=torch.float32, device="cuda")
+                for _ in range(2):
+                    Z = torch.addmm(C32, X, Y, out_dtype=torch.float32)
+                torch.cuda.synchronize()
+                ts = []
+                clk = bench.ClockSampler(0)
+                clk.__enter__()
+                for _ in range(40):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    Z = torch.addmm(C32, X, Y, out_dtype=torch.float32)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ts.append(e0.elapsed_time(e1) * 1e-3)
+                clk.__exit__(None, None, None)
+                t = statistics.median(ts)
+                print(json.dumps({"config": "config4", "impl": "cuBLAS (torch.addmm out_dtype=fp32) reference",
+                                  "dtype": dtype, "shape": [m, n, k], "seconds": t,
+                                  "tflops": 2.0 * m * n * k / t / 1e12, "output": "fp32 C + A·B (beta 1)",
+                                  "clocks": clk.summary()}), flush=True)
+                del C32
             del X, Y, Z
 
 
