@@ -1043,7 +1043,11 @@ cudaError_t launch_tma(Kernel kernel, const Args& args, int64_t M, int64_t N, in
     }
     Args local = args;
     local.prefetch_c = cmap ? 1 : 0;
-    if (const char* env = std::getenv("TILEMUL_TMA_PREFETCH_C")) local.prefetch_c &= std::atoi(env);
+    static const int prefetch_knob = [] {  // TILEMUL_TMA_PREFETCH_C=0: A/B knob
+        const char* env = std::getenv("TILEMUL_TMA_PREFETCH_C");
+        return env ? std::atoi(env) : 1;
+    }();
+    local.prefetch_c &= prefetch_knob;
     void* params[] = {&local, &ma, &mb, &mc};
     return cudaLaunchKernel(en.fn, dim3(grid), dim3(kTable[kernel].threads), params, en.smem, stream);
 }

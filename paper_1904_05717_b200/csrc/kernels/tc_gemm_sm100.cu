@@ -821,7 +821,11 @@ cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb,
         args.tma_c = g_encode(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-        if (const char* env = std::getenv("TILEMUL_TC_TMA_EPILOGUE")) args.tma_c &= std::atoi(env);
+        static const int tma_epilogue_knob = [] {  // TILEMUL_TC_TMA_EPILOGUE=0: A/B knob
+            const char* env = std::getenv("TILEMUL_TC_TMA_EPILOGUE");
+            return env ? std::atoi(env) : 1;
+        }();
+        args.tma_c &= tma_epilogue_knob;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
