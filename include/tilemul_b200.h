@@ -99,8 +99,10 @@ typedef struct {
      * reference. */
     int32_t parallel_loop;
     /* DMMA kernels: how the SMEM level is filled. TM_STAGING_AUTO picks TMA
-     * whenever it applies (16-byte aligned A/B and leading dimensions, every
-     * task's k range a whole number of slabs or ending at k), else cp.async. */
+     * for the 128x128 kernel when it applies (16-byte aligned A/B, leading
+     * dimensions and task origins; every task's k range a whole number of
+     * slabs or ending at k), launching a long task list in segments of whole
+     * rounds of at most 4096 k-slabs per CTA; else cp.async. Bitwise equal. */
     int32_t staging;
 } tm_exec_opts;
 enum { TM_STAGING_AUTO = 0, TM_STAGING_CPASYNC = 1, TM_STAGING_TMA = 2 };
