@@ -57,3 +57,28 @@ def test_validation_failure_carries_rules():
                      T.CacheHierarchy.from_capacities([64]), T.Shape(8, 8, 8))
     assert e.value.violations[0].rule == "resident_guest_exceed_capacity"
     assert e.value.violations[0].lhs == 10000 and e.value.violations[0].rhs == 64
+
+
+def test_cpp_shim_compiles_against_the_reference():
+    """include/tilemul_b200.hpp compiles after the reference's own headers
+    (checked where the reference tree exists, i.e. in the build container)."""
+    import shutil
+    import subprocess
+    import tempfile
+
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc) or shutil.which("g++") is None:
+        pytest.skip("reference headers or g++ absent")
+    inc = os.path.dirname(HEADER)
+    src = ('#include "tilemul/exec.hpp"\n#include "tilemul_b200.hpp"\n'
+           "void f(const tilemul::LoopNest& n, const tilemul::MatrixBuffer& a, const tilemul::MatrixBuffer& b,\n"
+           "       tilemul::MatrixBuffer& c, const tilemul::CacheHierarchy& h) {\n"
+           "    tilemul::b200::execute(n, a, b, c, h, {}, {TM_NUMERICS_EXACT});\n}\n")
+    with tempfile.NamedTemporaryFile("w", suffix=".cpp", delete=False) as f:
+        f.write(src)
+    try:
+        r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-I", ref_inc, "-I", inc,
+                            f.name], capture_output=True, text=True, timeout=120)
+    finally:
+        os.unlink(f.name)
+    assert r.returncode == 0 and "warning" not in r.stderr, r.stderr
