@@ -1,34 +1,42 @@
 #!/usr/bin/env python
-"""Benchmark of the hot path: one FP64 multilevel-blocked C += A·B per step.
+"""Benchmark of the hot path: one multilevel-blocked C += A·B per step.
 
-Workload (BASELINE.json configs[1], the largest square of the sweep that the
-metric is quoted on): m = n = k = 16384, FP64, column-major, A, B, C
-uniform[-1,1) from a seeded counter-based generator on the device (synthetic;
-the reference has no dataset), family member C2A1C0 lowered with the fused
-schedule onto the DMMA task kernel. Inputs are 6.4 GB (> 126 MB L2), so no
-L2 flush is needed between steps.
+Default workload (N = 1: BASELINE.json configs[1], the largest square of the
+sweep the metric is quoted on): m = n = k = 16384, FP64, column-major, A, B,
+C uniform[-1,1) from a seeded counter-based generator on the device
+(synthetic; the reference has no dataset), family member C2A1C0 lowered with
+the fused schedule onto the DMMA task kernel. Inputs are 6.4 GB (> 126 MB
+L2), so no L2 flush is needed between steps.
+
+N > 1 (torchrun): BASELINE.json configs[4], m = n = k = 65536 FP64 STRONG
+scaled -- C 2-D block-partitioned over a Pr x Pc grid (1x2, 2x2, 2x4), A
+row-panels / B column-panels exchanged in k-chunks under the local GEMMs
+(paper_1904_05717_b200/multigpu.py: copy-engine pulls over CUDA-IPC peer
+mappings, NCCL broadcasts as the fallback).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 1|2|3a|3b|3c|4|4tf32|5] [--size S]
+
+Every config of BASELINE.json can be run on request (`--config`); the
+default line is configs[1] at N = 1 and configs[4] at N > 1.
 
 One JSON line from rank 0. `value` = whole-job TFLOP/s with inputs resident
 in HBM (CUDA events on the launch stream, max over ranks); `e2e` = the same
-metric through the C ABI's host-buffer entry (tm_execute_host: pinned host
-A,B,C copied in, C copied out, inside the timed region); `roofline` = the
-task kernel's achieved FLOP/s over the FP64 DMMA peak measured live on this
-device; `cpu_baseline` = the reference's own execute() (oracle/_ref, built
-from the unmodified reference headers, -O2) on the host cores, on a bounded
-sub-problem. `--impl reference` times that same reference arm on the same
-config/metric.
-
-N > 1 (torchrun): the 2-D C partition of BASELINE configs[4] — each rank owns
-a 16384 x 16384 block of C (weak scaling), A row-panels and B column-panels
-are all-gathered over NCCL in k-chunks overlapped with the local GEMM.
+metric through the public API with host buffers (pinned host A, B, C copied
+in, C copied out, inside the timed region); `roofline` = the task kernel's
+achieved FLOP/s over the dtype's measured peak; `roofline.traffic` = DRAM
+bytes per launch from the committed ncu summary of this workload, ONLY when
+that summary was taken of this very build (build id) -- else null;
+`verified` = sampled entries of the timed run's own C against the oracle's
+restatement of the generator (outside the timed region; a miss exits 1);
+`cpu_baseline` = the reference's own execute() (oracle/_ref, built from the
+unmodified reference headers, -O2) on the host cores, on a bounded sample.
+`--impl reference` times that same reference arm on the same config/metric.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -42,28 +50,81 @@ sys.path.insert(0, ROOT)
 M = N = K = 16384
 FAMILY = "C2A1C0"
 METRIC = "GEMM TFLOP/s (FP64) and % of FP64 peak"  # both arms report this metric on this workload
+METRIC_TC = "GEMM TFLOP/s ({}) and % of tensor peak"
+
+# BASELINE.json configs: (m, n, k, family, C0 = zero?, dtype)
+CONFIGS = {
+    "1": (2048, 2048, 2048, "C2A1C0", True, "f64"),
+    "2": (16384, 16384, 16384, "C2A1C0", False, "f64"),
+    "3a": (16384, 16384, 256, "C2A1C0", False, "f64"),
+    "3b": (512, 512, 131072, "C2A1C0", False, "f64"),
+    "3c": (65536, 256, 1024, "B2A1C0", False, "f64"),
+    "4": (16384, 16384, 16384, "C2A1C0", True, "bf16"),
+    "4tf32": (16384, 16384, 16384, "C2A1C0", True, "tf32"),
+    "5": (65536, 65536, 65536, "C2A1C0", False, "f64"),
+}
+L2_BYTES = 126 * 2 ** 20
+VERIFY_SAMPLES = 64
 
 
-def workload_name(m):
-    return f"fp64 C+=A*B m=n=k={m} column-major, family {FAMILY} fused/DMMA"
+def workload_name(m, n=None, k=None, family=FAMILY, dtype="f64"):
+    n = m if n is None else n
+    k = m if k is None else k
+    shape = f"m=n=k={m}" if m == n == k else f"m={m} n={n} k={k}"
+    if dtype == "f64":
+        return f"fp64 C+=A*B {shape} column-major, family {family} fused/DMMA"
+    return f"{dtype} inputs, fp32 C+=A*B {shape} column-major, family {family} fused/tcgen05"
+
+
 CPU_SAMPLE = (2048, 2048, 8192)      # bounded sub-problem of the same workload for the CPU reference
 CPU_SAMPLE_REF_ARM = (2048, 2048, 4096)
 
 
-def parse():
+def cpu_sample(cfg, ref_arm=False):
+    """A bounded sub-problem of the config's workload for the CPU reference
+    (10-30 s of CPU work): config 1 runs whole (it is the reference's own
+    CPU-runnable case)."""
+    m, n, k = CONFIGS[cfg][:3]
+    if cfg == "1":
+        return (m, n, k)
+    if cfg == "3b":
+        return (512, 512, 16384)
+    if cfg == "3c":
+        return (4096, 256, 1024)
+    if cfg == "3a":
+        return (2048, 2048, 256)
+    return CPU_SAMPLE_REF_ARM if ref_arm else CPU_SAMPLE
+
+
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--size", type=int, default=M, help="square size (default 16384 = configs[1] max)")
+    p.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                   help="BASELINE.json config (default: 2 at N = 1, 5 at N > 1)")
+    p.add_argument("--size", type=int, default=None,
+                   help="square size override for configs 2 and 5 (default 16384 / 65536)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--staging", default="auto", choices=["auto", "cpasync", "tma"],
                    help="DMMA kernel staging (auto = TMA whenever it applies)")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-verify", action="store_true", help="skip the sampled-entry check (profiling runs only)")
     p.add_argument("--summa", action="store_true",
                    help="run the multi-GPU 2-D partition driver even at N=1 (exercises the N>1 code path)")
-    return p.parse_args()
+    a = p.parse_args(argv)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if a.config is None:
+        a.config = "5" if world > 1 else "2"
+    return a
+
+
+def shape_of(args):
+    m, n, k, family, c0_zero, dtype = CONFIGS[args.config]
+    if args.size and args.config in ("2", "5"):
+        m = n = k = args.size
+    return m, n, k, family, c0_zero, dtype
 
 
 # ----------------------------------------------------------------- helpers
@@ -92,7 +153,7 @@ def host_hierarchy():
     return caps
 
 
-def cpu_reference_run(shape, reps, workers):
+def cpu_reference_run(shape, reps, workers, family=FAMILY):
     """The reference's own execute() (oracle/_ref) on host buffers; returns
     (TFLOP/s, seconds per rep, blocksizes)."""
     from oracle import oracle as O
@@ -101,15 +162,33 @@ def cpu_reference_run(shape, reps, workers):
         raise FileNotFoundError("oracle/_ref/libtilemul_ref.so not built")
     m, n, k = shape
     caps = host_hierarchy()
-    rc, bs = O.ref_derive(FAMILY, caps, shape)
+    rc, bs = O.ref_derive(family, caps, shape)
     if rc != 0:
         raise RuntimeError(f"reference derive failed: {bs}")
     a, b, c = O.fill_uniform(7, [(m, k), (k, n), (m, n)])
     secs = []
     for _ in range(reps):
-        secs.append(O.ref_execute(FAMILY, caps, shape, bs, a, b, c, workers=workers))
+        secs.append(O.ref_execute(family, caps, shape, bs, a, b, c, workers=workers))
     t = statistics.median(secs)
     return 2.0 * m * n * k / t / 1e12, t, bs, caps
+
+
+def cpu_baseline_leg(cfg, family, dtype):
+    """The cpu_baseline object: the reference's execute() on all host cores
+    on the config's bounded sample; errors are reported, never replaced."""
+    shape = cpu_sample(cfg)
+    workers = os.cpu_count() or 1
+    try:
+        tf, t, cbs, caps = cpu_reference_run(shape, 3 if cfg != "1" else 2, workers, family)
+        what = "" if dtype == "f64" else f" (FP64: the reference has no {dtype} path; same flops)"
+        return {"value": tf, "unit": "TFLOP/s", "cores": workers, "kind": "reference",
+                "sample": f"reference execute() {family}{what}, {shape[0]}x{shape[1]}x{shape[2]} "
+                          f"{'(the whole config)' if cfg == '1' else 'sub-problem of the same workload'}, "
+                          f"median of reps ({t:.2f} s each), host hierarchy {caps} elements, -O2 unmodified "
+                          f"reference headers"}
+    except Exception as exc:  # reported, never silently replaced
+        return {"value": None, "unit": "TFLOP/s", "cores": workers, "kind": "reference",
+                "sample": f"unavailable: {exc}"}
 
 
 class ClockSampler:
@@ -148,7 +227,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], 0, set()
+        sm, mx, reasons, power = [], 0, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -157,29 +236,49 @@ class ClockSampler:
             try:
                 sm.append(float(f[0]))
                 mx = max(mx, float(f[1]))
+                power.append(float(f[2]))
             except ValueError:
                 continue
             for nm, v in zip(names, f[4:8]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": statistics.median(power) if power else None}
 
 
-def ncu_traffic(workload, staging="cpasync"):
-    """Per-launch DRAM bytes of the task kernel from the committed ncu
-    --set full summary of this workload and staging (profiles/), or None."""
-    for name in sorted(os.listdir(os.path.join(ROOT, "profiles")), reverse=True) if os.path.isdir(
-            os.path.join(ROOT, "profiles")) else []:
-        if name.startswith("ncu_summary") and name.endswith(".json"):
-            try:
-                d = json.load(open(os.path.join(ROOT, "profiles", name)))
-            except (OSError, ValueError):
-                continue
-            if d.get("workload") == workload and d.get("staging", "cpasync") == staging and d.get(
-                    "dram_bytes_per_launch"):
-                return d["dram_bytes_per_launch"], name
-    return None, None
+def ncu_traffic(workload, staging, launches_per_step):
+    """DRAM bytes per launch (and per step) of the task kernel from the
+    committed ncu --set full summary of this workload and staging -- only if
+    that summary was captured from THIS build (its build id equals the loaded
+    library's) with the same launches per step. Otherwise (None, reason)."""
+    from paper_1904_05717_b200 import _native
+
+    bid = _native.build_id()
+    pdir = os.path.join(ROOT, "profiles")
+    stale = None
+    for name in sorted(os.listdir(pdir), reverse=True) if os.path.isdir(pdir) else []:
+        if not (name.startswith("ncu_summary") and name.endswith(".json")):
+            continue
+        try:
+            d = json.load(open(os.path.join(pdir, name)))
+        except (OSError, ValueError):
+            continue
+        if d.get("workload") != workload or d.get("staging", "cpasync") != staging:
+            continue
+        if d.get("build_id") != bid or d.get("launches_per_step") != launches_per_step or not d.get(
+                "dram_bytes_per_step"):
+            stale = stale or f"{name}: build {d.get('build_id')} / {d.get('launches_per_step')} launches per step"
+            continue
+        return {"per_launch": d["dram_bytes_per_step"] / launches_per_step, "per_step": d["dram_bytes_per_step"],
+                "source": name, "build_id": bid}
+    return {"per_launch": None, "per_step": None, "source": None, "build_id": bid,
+            "why_null": (f"no ncu summary of build {bid} for this workload"
+                         + (f" (stale: {stale})" if stale else ""))}
+
+
+def flush_l2(buf):
+    buf.zero_()  # a 512 MB write evicts the 126 MB L2 (between timed steps, outside their events)
 
 
 # ------------------------------------------------------------ reference arm
@@ -188,28 +287,34 @@ def reference_arm(args):
     if rank != 0:
         return 0
     workers = os.cpu_count() or 1
-    shape = CPU_SAMPLE_REF_ARM
+    m, n, k, family, _, dtype = shape_of(args)
+    shape = cpu_sample(args.config, ref_arm=True)
     from oracle import oracle as O
 
     if not O.have_ref():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtilemul_ref.so was not built"}))
         return 0
     for _ in range(args.warmup):
-        cpu_reference_run(shape, 1, workers)
+        cpu_reference_run(shape, 1, workers, family)
     times = []
+    bs = None
     for _ in range(args.steps):
-        tf, t, bs, caps = cpu_reference_run(shape, 1, workers)
+        tf, t, bs, caps = cpu_reference_run(shape, 1, workers, family)
         times.append(t)
     total = sum(times)
     flops = 2.0 * shape[0] * shape[1] * shape[2]
     value = flops * len(times) / total / 1e12
-    sample = (f"reference execute() {FAMILY} on the {shape[0]}x{shape[1]}x{shape[2]} sub-problem of the "
-              f"{M}^3 workload per step, host-derived blocksizes {sorted(bs.items())}, -O2 reference build")
+    sample = (f"reference execute() {family} on the {shape[0]}x{shape[1]}x{shape[2]} "
+              f"{'config (whole)' if tuple(shape) == (m, n, k) else 'sub-problem of the workload'} per step, "
+              f"host-derived blocksizes {sorted(bs.items())}, -O2 reference build, {workers} threads"
+              + ("" if dtype == "f64" else f"; FP64 (the reference has no {dtype} path)"))
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "impl": "reference", "metric": METRIC if dtype == "f64" else METRIC_TC.format(dtype), "value": value,
+        "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.size), "sample": list(shape)},
+        "higher_is_better": True, "scaling": "strong" if args.config == "5" else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(m, n, k, family, dtype), "sample": list(shape)},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": workers, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -218,78 +323,107 @@ def reference_arm(args):
 
 
 # ------------------------------------------------------------------ our arm
-def make_plan(T, m, n, k, tile=128):
-    """C2A1C0 on the B200 hierarchy with the L2 level at its effective
-    capacity for residency (planner.L2_EFFECTIVE, measured), blocksizes from
-    the reference's derivation with the GPU pins (planner.derive_for_gpu)."""
+def make_plan(T, m, n, k, tile=128, family=FAMILY):
+    """The family member on the B200 hierarchy with the L2 level at its
+    effective capacity for residency (planner), blocksizes from the
+    reference's derivation with the GPU pins (planner.derive_for_gpu)."""
     from paper_1904_05717_b200 import planner as P
 
     hier = P.gpu_hierarchy_effective(tile)
-    bs = P.derive_for_gpu(FAMILY, (m, n, k), hier, (tile, tile))
-    return T.build_plan(T.parse_name(FAMILY), bs, hier, T.Shape(m, n, k)), bs, hier
+    bs = P.derive_for_gpu(family, (m, n, k), hier, (tile, tile))
+    return T.build_plan(T.parse_name(family), bs, hier, T.Shape(m, n, k)), bs, hier
 
 
-def our_arm(args):
+def verify_sampled(C, m, n, k, steps, seeds, c0_zero, samples=VERIFY_SAMPLES, a_round=None, ld=None,
+                   row0=0, col0=0, gm=None, gk=None):
+    """PARITY CHECK, outside every timed region: `samples` entries of the
+    timed run's own C (C0 + steps·A·B, every step on the same inputs) against
+    the oracle's restatement of the device generator (oracle.counter_entries;
+    nothing read back from the GPU feeds the expected values). Bound:
+    4(steps·k+1)u(steps·|A||B| + |C0|), u = 2^-53 (fp64) or (steps·k+2)·2^-24
+    (tensor cores, fp32 accumulate of rounded inputs)."""
+    import numpy as np
     import torch
-    import torch.distributed as dist
+
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(2026)
+    ii, jj = rng.integers(0, m, samples), rng.integers(0, n, samples)
+    ld = ld or m
+    got = C[torch.from_numpy(ii + jj * ld).to(C.device)].double().cpu().numpy()
+    want, ab, c0 = O.counter_entries(k, ii, jj, seeds=seeds, lda=gm or m, ldb=gk or k, ldc=gm or m, row0=row0,
+                                     col0=col0, steps=steps, a_round=a_round, c0=not c0_zero)
+    if a_round:
+        bound = (steps * k + 2) * 2.0 ** -24 * (steps * ab + np.abs(c0))
+    else:
+        bound = 4.0 * (steps * k + 1) * 2.0 ** -53 * (steps * ab + np.abs(c0))
+    ratio = np.abs(got - want) / np.where(bound > 0, bound, 1.0)
+    return {"samples": int(samples), "ok": bool(np.all(ratio <= 1.0)), "worst_err_over_bound": float(np.max(ratio)),
+            "bound": "4(s*k+1)u(s|A||B|+|C0|), u=2^-53" if not a_round else "(s*k+2)2^-24(s|A||B|+|C0|)",
+            "steps_accumulated": steps, "oracle": "oracle.counter_entries (generator restated on the host)"}
+
+
+def fp64_arm(args):
+    import torch
 
     from paper_1904_05717_b200 import tilemul as T
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1 or args.summa:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29541")
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
-        from paper_1904_05717_b200 import multigpu
-
-        return multigpu.bench(args, T, make_plan, world, rank, local)
-
-    m = n = k = args.size
-    nest, bs, hier = make_plan(T, m, n, k)
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    m, n, k, family, c0_zero, _ = shape_of(args)
+    nest, bs, hier = make_plan(T, m, n, k, family=family)
     stream = torch.cuda.current_stream()
     A = torch.empty(m * k, dtype=torch.float64, device="cuda")
     B = torch.empty(k * n, dtype=torch.float64, device="cuda")
     C = torch.empty(m * n, dtype=torch.float64, device="cuda")
     T.fill_uniform_device(A, 1)
     T.fill_uniform_device(B, 2)
-    T.fill_uniform_device(C, 3)
-    # auto split_k: only the last partial wave's tiles are k-split (tail split)
+    if c0_zero:
+        C.zero_()
+    else:
+        T.fill_uniform_device(C, 3)
+    in_bytes = 8 * (m * k + k * n + m * n)
+    flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device="cuda") if in_bytes < 4 * L2_BYTES else None
+    # auto split_k: tail split of the last partial wave, or stream-K on a ragged few-wave grid
     opts = T.ExecOptions(numerics="dmma", schedule="fused", split_k=0, staging=args.staging)
     for _ in range(args.warmup):
         T.execute(nest, A, B, C, opts)
     torch.cuda.synchronize()
     launches_per_step = nest.last_launch()["launches"]
     staging = nest.last_launch()["staging"]
+    tile = "128x128"
     kernel_name = ("k_dmma_tma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3> (16 warps, TMA 128B-swizzled slabs"
-                   + (f"; {launches_per_step} launches per step, segments of whole rounds" if launches_per_step > 1 else "")
-                   + ")" if staging == "tma" else
-                   "k_dmma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3,vec16> (16 warps, cp.async)")
+                   + (f"; {launches_per_step} launches per step, segments of whole rounds" if launches_per_step > 1
+                      else "") + ")" if staging == "tma" else
+                   f"k_dmma (cp.async staging, {launches_per_step} launch(es) per step)")
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
         torch.cuda.synchronize()
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for i in range(args.steps):
+            if flush is not None:
+                flush_l2(flush)
             ev[i][0].record(stream)
             T.execute(nest, A, B, C, opts)
             ev[i][1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
-    total_ms = t_start.elapsed_time(t_end)
     step_ms = [s.elapsed_time(e) for s, e in ev]
+    total_ms = sum(step_ms) if flush is not None else t_start.elapsed_time(t_end)
     flops = 2.0 * m * n * k
     value = flops * args.steps / (total_ms * 1e-3) / 1e12
-    kernel_ms = sum(step_ms) / len(step_ms)  # per step: the task kernel (+ a tile reduction when tail-split)
+    kernel_ms = sum(step_ms) / len(step_ms)  # per step: the task kernel launch(es)
     achieved = flops / (kernel_ms * 1e-3) / 1e12
 
+    verified = None
+    if not args.no_verify:
+        verified = verify_sampled(C, m, n, k, args.warmup + args.steps, (1, 2, 3), c0_zero)
+
     peak = T.measure_fp64_peak(30)
-    workload = workload_name(m)
-    traffic, traffic_src = ncu_traffic(workload, staging)
+    workload = workload_name(m, n, k, family)
+    traffic = ncu_traffic(workload, staging, launches_per_step)
     model = nest.model()
     hbm_model_bytes = model.at_level(hier.top_level()).total_bytes()
 
@@ -307,59 +441,184 @@ def our_arm(args):
         dt = (time.perf_counter() - t0) / e2e_steps
         e2e = {"value": flops / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 8 * (m * k + k * n + m * n),
                "d2h_bytes_per_step": 8 * m * n, "ms_per_step": dt * 1e3,
-               "path": "tm_execute_host (pinned host A,B,C -> device, C back; one persistent launch fed by the copy engine)"}
+               "path": "tilemul.execute on host arrays -> tm_execute_host (pinned host A,B,C -> device, C back; "
+                       "one persistent launch fed by the copy engine); host wall clock around the synchronous call"}
         del Ah, Bh, Ch
 
-    # ---- CPU baseline: the reference's execute() on the host cores
-    cpu = None
-    if not args.no_cpu:
-        try:
-            workers = os.cpu_count() or 1
-            tf, t, cbs, caps = cpu_reference_run(CPU_SAMPLE, 3, workers)
-            cpu = {"value": tf, "unit": "TFLOP/s", "cores": workers, "kind": "reference",
-                   "sample": f"reference execute() {FAMILY}, {CPU_SAMPLE[0]}x{CPU_SAMPLE[1]}x{CPU_SAMPLE[2]} "
-                             f"sub-problem of the same workload, median of 3 ({t:.2f} s each), host hierarchy "
-                             f"{caps} elements, -O2 unmodified reference headers"}
-        except Exception as exc:  # reported, never silently replaced
-            cpu = {"value": None, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"unavailable: {exc}"}
-
+    cpu = None if args.no_cpu else cpu_baseline_leg(args.config, family, "f64")
+    flush_note = ("512 MB buffer written between timed steps (outside their events): inputs "
+                  f"{in_bytes / 1e6:.0f} MB < 4x L2" if flush is not None else
+                  f"not needed: inputs {in_bytes / 1e9:.2f} GB >> 126 MB L2")
     out = {
         "metric": METRIC,
         "value": value, "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded counter-based uniform[-1,1) on device)",
-        "config": {"workload": workload, "m": m, "n": n, "k": k, "family": FAMILY,
+        "config": {"workload": workload, "baseline_config": args.config, "m": m, "n": n, "k": k, "family": family,
+                   "c0": "zero" if c0_zero else "uniform[-1,1)",
                    "blocksizes": {f"{lv}:{d}": v for (lv, d), v in bs.entries()},
-                   "schedule": "fused", "numerics": "dmma (mma.sync m8n8k4 f64)", "cta_tile": "128x128",
-                   "staging": staging,
-                   "split_k": "auto (tail split of the last partial wave)",
-                   "l2_flush": "not needed: inputs 6.4 GB > 126 MB L2", "parallelism": "1 GPU",
-                   "hierarchy_elements": [hier.capacity(i) for i in range(hier.size())],
-                   "l2_effective_fraction": 0.25},
+                   "schedule": "fused", "numerics": "dmma (mma.sync m8n8k4 f64)", "cta_tile": tile,
+                   "staging": staging, "split_k": "auto (tail split / stream-K)",
+                   "l2_flush": flush_note, "parallelism": "1 GPU",
+                   "hierarchy_elements": [hier.capacity(i) for i in range(hier.size())]},
         "pct_of_fp64_peak": 100.0 * value / peak,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak, "traffic": traffic["per_launch"],
                      "peak_source": "FP64 DMMA issue-rate probe run live in this bench (MEASURED_PEAKS.json has no "
                                     "FP64 figure); nominal 148 SM x 64 FMA/clk x 1.965 GHz = 37.2",
                      "kernel": kernel_name, "algorithmic_flops_per_launch": flops / launches_per_step,
                      "algorithmic_flops_per_step": flops, "launches_per_step": launches_per_step,
-                     "traffic_source": traffic_src},
+                     "traffic_per_step": traffic["per_step"], "traffic_source": traffic["source"],
+                     "build_id": traffic["build_id"], **({"traffic_null_because": traffic["why_null"]}
+                                                         if traffic["per_launch"] is None else {})},
         "model": {"hbm_bytes_model": hbm_model_bytes,
-                  "hbm_bytes_measured": traffic,
-                  "measured_over_model": (traffic / hbm_model_bytes) if traffic else None},
+                  "hbm_bytes_measured": traffic["per_step"],
+                  "measured_over_model": (traffic["per_step"] / hbm_model_bytes) if traffic["per_step"] else None},
+        "verified": verified,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": launches_per_step * args.steps,
         "step_ms": step_ms,
     }
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
+    if verified is not None and not verified["ok"]:
+        print(f"PARITY FAILURE: sampled entries outside the bound: {verified}", file=sys.stderr)
+        return 1
     return 0
 
 
-def main():
-    args = parse()
+def tc_arm(args):
+    """Config 4: BF16 (or TF32) inputs RNE-rounded from uniform[-1,1) FP64,
+    fp32 C += A·B on the tcgen05 SM-pair kernel (256 x 512 per pair)."""
+    import torch
+
+    from paper_1904_05717_b200 import tilemul as T
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    m, n, k, family, _, dtype = shape_of(args)
+    hier = T.CacheHierarchy.from_capacities([256 * 512, 232448, 132644864 // 2])
+    d = T.parse_name(family)
+    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(256, 512)),
+                             pinned=T.BlocksizeSet({(1, "m"): 256}))
+    nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+    x = torch.empty(m * k, dtype=torch.float64, device="cuda")
+    T.fill_uniform_device(x, 31)
+    A = T.round_inputs(x, dtype)
+    x = torch.empty(k * n, dtype=torch.float64, device="cuda")
+    T.fill_uniform_device(x, 32)
+    B = T.round_inputs(x, dtype)
+    del x
+    C = torch.zeros(m * n, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        T.execute_tc(nest, A, B, C, dtype)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            T.execute_tc(nest, A, B, C, dtype)
+            ev[i][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    flops = 2.0 * m * n * k
+    value = flops * args.steps / (total_ms * 1e-3) / 1e12
+    achieved = flops / (sum(step_ms) / len(step_ms) * 1e-3) / 1e12
+    verified = None
+    if not args.no_verify:
+        verified = verify_sampled(C, m, n, k, args.warmup + args.steps, (31, 32, 0), True,
+                                  a_round=8 if dtype == "bf16" else 11)
+    probe = T.measure_tc_peak(dtype, 5)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    if dtype == "bf16" and peaks.get("bf16_tflops_sustained"):
+        peak, src = peaks["bf16_tflops_sustained"], "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS, back to back)"
+    elif dtype == "tf32" and peaks.get("bf16_tflops_sustained"):
+        peak, src = peaks["bf16_tflops_sustained"] / 2, "MEASURED_PEAKS.json bf16_tflops_sustained / 2 (tf32 rate)"
+    else:
+        peak, src = probe, "tcgen05 issue-rate probe (live)"
+    workload = workload_name(m, n, k, family, dtype)
+    traffic = ncu_traffic(workload, "tma", 1)
+    e2e = None
+    if not args.no_e2e:
+        Ah, Bh = A.cpu().pin_memory(), B.cpu().pin_memory()
+        Ch = C.cpu().pin_memory()
+        Ad, Bd, Cd = torch.empty_like(A), torch.empty_like(B), torch.empty_like(C)
+        steps = max(1, min(args.steps, 3))
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(steps):
+            Ad.copy_(Ah, non_blocking=True)
+            Bd.copy_(Bh, non_blocking=True)
+            Cd.copy_(Ch, non_blocking=True)
+            T.execute_tc(nest, Ad, Bd, Cd, dtype)
+            Ch.copy_(Cd, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te = f0.elapsed_time(f1) / steps
+        eb = A.element_size()
+        e2e = {"value": flops / (te * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": te,
+               "h2d_bytes_per_step": eb * (m * k + k * n) + 4 * m * n, "d2h_bytes_per_step": 4 * m * n,
+               "path": "pinned host A, B (rounded), C (fp32) copied in, tilemul.execute_tc, C copied out"}
+    cpu = None if args.no_cpu else cpu_baseline_leg(args.config, family, dtype)
+    out = {
+        "metric": METRIC_TC.format(dtype), "value": value, "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded counter-based uniform[-1,1), RNE-rounded)",
+        "config": {"workload": workload, "baseline_config": args.config, "m": m, "n": n, "k": k, "family": family,
+                   "c0": "zero (config 4 leaves C init unspecified)", "accumulate": "fp32 (TMEM)",
+                   "cta_tile": "256x512 per SM pair (cta_group::2)", "l2_flush": "not needed: inputs > 1.5 GB",
+                   "parallelism": "1 GPU"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic["per_launch"], "peak_source": src,
+                     "tcgen05_issue_probe_tflops": probe, "kernel": "k_tc2<%s, 2> (256x512 SM pair, TMA epilogue)" % dtype,
+                     "algorithmic_flops_per_launch": flops, "traffic_source": traffic["source"],
+                     "build_id": traffic["build_id"]},
+        "verified": verified, "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
+        "gpu_launches": args.steps, "step_ms": step_ms,
+    }
+    print(json.dumps(out), flush=True)
+    if verified is not None and not verified["ok"]:
+        print(f"PARITY FAILURE: sampled entries outside the bound: {verified}", file=sys.stderr)
+        return 1
+    return 0
+
+
+def our_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1904_05717_b200 import tilemul as T
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1 or args.summa or args.config == "5":
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29541")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        from paper_1904_05717_b200 import multigpu
+
+        return multigpu.bench(args, T, make_plan, world, rank, local)
+    if CONFIGS[args.config][5] != "f64":
+        return tc_arm(args)
+    return fp64_arm(args)
+
+
+def main(argv=None):
+    args = parse(argv)
     if args.impl == "reference":
         return reference_arm(args)
     return our_arm(args)

@@ -114,6 +114,9 @@ const char* tm_last_error(void);
 /* Rule ids of the last failure, one per line "rule:level:lhs:rhs". */
 const char* tm_last_rules(void);
 const char* tm_version(void);
+/* sha256[:16] of the sources this library was built from (build.py
+ * source_hash); ncu summaries under profiles/ carry the id they measured. */
+const char* tm_build_id(void);
 
 /* --- family descriptors (include/tilemul/descriptor.hpp) ---------------- */
 /* parse_name (:111-125): fills up to `cap` tiers, sets *count. */

@@ -272,6 +272,46 @@ def counter_uniform(seed: int, index):
     return 2.0 * u - 1.0
 
 
+def round_rne(x, bits: int):
+    """x (float64) rounded to `bits` significant bits, round-to-nearest-even,
+    in one step (no double rounding through fp32): bf16 = 8 bits, TF32 = 11.
+    The restatement of the device's k_round_bf16 / k_round_tf32 for values in
+    the normal range of fp32 (every uniform[-1,1) input)."""
+    x = np.asarray(x, dtype=np.float64)
+    mant, ex = np.frexp(x)                      # x = mant * 2^ex, 0.5 <= |mant| < 1
+    return np.ldexp(np.rint(np.ldexp(mant, bits)), ex - bits)  # np.rint: half to even
+
+
+def counter_entries(k, ii, jj, seeds=(1, 2, 3), lda=None, ldb=None, ldc=None, row0=0, col0=0, steps=1,
+                    a_round=None, c0=True):
+    """Sampled entries of C = C0 + steps·A·B where A (lda-strided, column-major),
+    B and C0 are the device's counter-based fills (tm_fill_uniform_*, restated
+    by counter_uniform) over GLOBAL indices: A(i, p) = u(seeds[0], i + p·lda),
+    B(p, j) = u(seeds[1], p + j·ldb), C0(i, j) = u(seeds[2], i + j·ldc);
+    (ii, jj) are local indices offset by (row0, col0). Nothing is read back
+    from the GPU: the inputs are regenerated here.
+
+    a_round (bits): round A and B as the tensor-core path does (round_rne).
+    Returns (want, absprod, c0) for the bound 4(steps·k+1)u(steps·|A||B| + |C0|):
+    want = c0 + steps·Σ_p a·b, summed sequentially in ascending p (or_entries)."""
+    ii = np.asarray(ii, dtype=np.int64)
+    jj = np.asarray(jj, dtype=np.int64)
+    S = ii.size
+    gi = (ii + row0).astype(np.uint64)
+    gj = (jj + col0).astype(np.uint64)
+    p = np.arange(k, dtype=np.uint64)
+    rows = counter_uniform(seeds[0], gi[:, None] + p[None, :] * np.uint64(lda))     # (S, k)
+    cols = counter_uniform(seeds[1], p[None, :] + gj[:, None] * np.uint64(ldb))     # (S, k)
+    if a_round:
+        rows, cols = round_rne(rows, a_round), round_rne(cols, a_round)
+    a_s = np.asfortranarray(rows).ravel(order="F")   # S x k column-major: a_s[t + p*S]
+    b_s = np.ascontiguousarray(cols).ravel()          # k x S column-major: b_s[p + t*k]
+    t = np.arange(S, dtype=np.int64)
+    dot, ab = entries(k, a_s, S, b_s, k, None, S, t, t)
+    cz = counter_uniform(seeds[2], gi + gj * np.uint64(ldc)) if c0 else np.zeros(S)
+    return cz + steps * dot, ab, cz
+
+
 def ref_pack(name, caps, shape, bs, op, src, inclusive=None):
     """The reference's pack(src, nest) of operand `op` (column-major -> layout_for)."""
     L = ref()

@@ -10,7 +10,8 @@ import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 # TILEMUL_B200_LIB: load another build of the library (A/B kernel experiments)
-LIB_PATH = os.environ.get("TILEMUL_B200_LIB") or os.path.join(PKG, "lib", "libtilemul_b200.so")
+DEFAULT_LIB = os.path.join(PKG, "lib", "libtilemul_b200.so")
+LIB_PATH = os.environ.get("TILEMUL_B200_LIB") or DEFAULT_LIB
 
 
 class tm_level(C.Structure):
@@ -55,6 +56,7 @@ SIGNATURES = [
     ("tm_last_error", cstr, []),
     ("tm_last_rules", cstr, []),
     ("tm_version", cstr, []),
+    ("tm_build_id", cstr, []),
     ("tm_parse_name", C.c_int, [cstr, C.c_int, C.POINTER(tm_tier), C.c_int, C.POINTER(C.c_int)]),
     ("tm_compose", C.c_int, [C.POINTER(i32), cstr, C.c_int, C.c_int, C.c_char_p, C.c_int, C.POINTER(tm_tier), C.c_int,
                              C.POINTER(C.c_int)]),
@@ -120,8 +122,20 @@ def lib():
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
+        if LIB_PATH == DEFAULT_LIB:
+            from . import build as _b
+
+            want, have = _b.source_hash(), L.tm_build_id().decode()
+            if want != have:
+                raise ImportError(f"{LIB_PATH} was built from other sources (build id {have}, sources {want}): "
+                                  "rebuild with `python -m paper_1904_05717_b200.build`")
         _lib = L
     return _lib
+
+
+def build_id() -> str:
+    """The loaded library's build id (sha256[:16] of its sources)."""
+    return lib().tm_build_id().decode()
 
 
 def declared_symbols():

@@ -25,7 +25,7 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXFLAGS = ["-std=c++17", "-O2", "-fPIC", "-Wall", "-Wno-unused-function", f"-I{CUDA_HOME}/include",
-            f"-I{os.path.join(ROOT, 'include')}"]
+            f"-I{os.path.join(ROOT, 'include')}", f"-I{OBJ}"]
 NVFLAGS = ARCH + ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                   f"-I{os.path.join(ROOT, 'include')}"] + os.environ.get("TILEMUL_B200_NVFLAGS", "").split()
 
@@ -33,6 +33,37 @@ NVFLAGS = ARCH + ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--ex
 def _headers():
     return glob.glob(os.path.join(CSRC, "**", "*.hpp"), recursive=True) + [
         os.path.join(ROOT, "include", "tilemul_b200.h")]
+
+
+BUILD_ID = os.path.join(OBJ, "build_id.h")
+
+
+def source_files():
+    """Every file the library is built from (the build id hashes these)."""
+    return sorted(glob.glob(os.path.join(CSRC, "**", "*.cpp"), recursive=True) +
+                  glob.glob(os.path.join(CSRC, "**", "*.cu"), recursive=True) +
+                  glob.glob(os.path.join(CSRC, "**", "*.hpp"), recursive=True) +
+                  [os.path.join(ROOT, "include", "tilemul_b200.h"), os.path.abspath(__file__)])
+
+
+def source_hash() -> str:
+    """sha256[:16] over the library's sources (paths relative to the repo,
+    then contents): the build id compiled into the library (tm_build_id) and
+    stamped on every ncu summary, so a profile of another build is detected."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in source_files():
+        h.update(os.path.relpath(f, ROOT).replace(os.sep, "/").encode() + b"\0")
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
+
+
+def _write_build_id() -> None:
+    text = f'#pragma once\n#define TM_BUILD_ID "{source_hash()}"\n'
+    if not os.path.exists(BUILD_ID) or open(BUILD_ID).read() != text:
+        with open(BUILD_ID, "w") as f:
+            f.write(text)
 
 
 def _stale(target, deps):
@@ -45,7 +76,7 @@ def _stale(target, deps):
 def _compile(src):
     rel = os.path.relpath(src, CSRC).replace(os.sep, "_")
     obj = os.path.join(OBJ, rel + ".o")
-    if not _stale(obj, [src] + _headers()):
+    if not _stale(obj, [src] + _headers() + ([BUILD_ID] if src.endswith("capi.cpp") else [])):
         return obj, None
     if src.endswith(".cu"):
         cmd = [NVCC] + NVFLAGS + ["-c", src, "-o", obj]
@@ -62,6 +93,7 @@ def build(verbose: bool = False) -> str:
     os.makedirs(LIB_DIR, exist_ok=True)
     if not os.path.exists(NVCC) and shutil.which("nvcc") is None:
         raise RuntimeError("nvcc not found; cannot build the sm_100a kernels")
+    _write_build_id()
     srcs = sorted(glob.glob(os.path.join(CSRC, "**", "*.cpp"), recursive=True) +
                   glob.glob(os.path.join(CSRC, "**", "*.cu"), recursive=True))
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:

@@ -480,10 +480,16 @@ def fill_local(lay: Layout, rank: int, A_local, B_local, C_local, fill_block, se
 
 # ----------------------------------------------------------------- bench
 def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
-    """bench.py at N > 1 (or --summa): weak scaling, each rank owns a
-    size x size block of C with K = size; value = total flops / max-over-ranks
-    time. e2e: every rank copies its A/B/C pieces from pinned host memory,
-    runs, and copies its C block back inside the timed region."""
+    """bench.py at N > 1 (or --config 5 / --summa at N = 1).
+
+    config 5 (the default at N > 1, BASELINE.json configs[4]): m = n = k =
+    S = 65536 STRONG scaled -- the fixed global problem is cut into a
+    Pr x Pc grid of (S/Pr) x (S/Pc) C blocks; value = 2S^3 / max-over-ranks
+    step time, so value(N) / (N * value(1)) is T1 / (P * T_P).
+    --summa with config 2: weak scaling, each rank owns a size x size C block
+    with K = size.
+    e2e: every rank copies its A/B/C pieces from pinned host memory, runs, and
+    copies its C block back inside the timed region."""
     import json
 
     import torch
@@ -491,8 +497,15 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
 
     import bench as B0
 
-    size = args.size
-    lay = make_layout(world, size, size, size)
+    cfg = getattr(args, "config", None) or ("5" if world > 1 else "2")
+    strong = cfg == "5"
+    if strong:
+        S = getattr(args, "size", None) or 65536
+        pr, pc = grid_shape(world)
+        lay = make_layout(world, S // pr, S // pc, S)
+    else:
+        size = getattr(args, "size", None) or 16384
+        lay = make_layout(world, size, size, size)
     rows, cols = Summa.groups(dist, lay)
     r, c = lay.coords(rank)
     dev = torch.device("cuda", local)
@@ -533,6 +546,18 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
     flops = 2.0 * lay.M * lay.N * lay.K * args.steps
     per_gpu = flops / world / t / 1e12
 
+    # parity check of the timed run's own C block on every rank (outside the timed region)
+    verified = None
+    if not getattr(args, "no_verify", False):
+        v = B0.verify_sampled(C, lay.mL, lay.nL, lay.K, args.warmup + args.steps, (11, 12, 13), False,
+                              row0=r * lay.mL, col0=c * lay.nL, gm=lay.M, gk=lay.K)
+        flag = torch.tensor([1.0 if v["ok"] else 0.0, v["worst_err_over_bound"]], dtype=torch.float64, device=dev)
+        lo = flag.clone()
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        verified = dict(v, ok=bool(lo[0].item() == 1.0), worst_err_over_bound=float(flag[1].item()),
+                        samples=v["samples"] * world, ranks=world)
+
     e2e = None
     e2e_exchange = exchange
     if s.peer_a is not None and not args.no_e2e:
@@ -541,7 +566,19 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
         else:
             s.detach_peers()  # no cross-process events: the e2e step exchanges with the broadcasts
             e2e_exchange = "nccl broadcasts (step events unavailable)"
+    e2e_skip = None
     if not args.no_e2e:
+        need = 8 * (A.numel() + B.numel() + C.numel()) * world  # pinned host copies of every rank's pieces
+        try:
+            import psutil
+
+            avail = psutil.virtual_memory().available
+        except Exception:  # noqa: BLE001
+            avail = None
+        if avail is not None and need > 0.6 * avail:
+            e2e_skip = (f"pinned host pieces of all ranks need {need / 1e9:.0f} GB, the host has "
+                        f"{avail / 1e9:.0f} GB available")
+    if not args.no_e2e and e2e_skip is None:
         Ah, Bh, Ch = (x.cpu().pin_memory() for x in (A, B, C))
         steps = max(1, min(args.steps, 3))
         hs = HostStep(s, A, B, C, lambda w: make_plan(T, lay.mL, w, lay.KC)[0],
@@ -573,10 +610,15 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
         print(json.dumps({
             "metric": "GEMM TFLOP/s (FP64) and % of FP64 peak", "value": flops / t / 1e12, "unit": "TFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "dtype": "f64",
             "data": "synthetic (seeded counter-based uniform[-1,1), generated per rank from global indices)",
-            "config": {"workload": f"fp64 C+=A*B, C 2-D partitioned {lay.Pr}x{lay.Pc}, local {lay.mL}x{lay.nL}, "
-                                   f"K={lay.K}, family C2A1C0 fused/DMMA", "grid": [lay.Pr, lay.Pc],
+            "config": {"workload": (B0.workload_name(lay.M, lay.N, lay.K) + f" (BASELINE config 5), C 2-D partitioned "
+                                    f"{lay.Pr}x{lay.Pc}" if strong else
+                                    f"fp64 C+=A*B, C 2-D partitioned {lay.Pr}x{lay.Pc}, local {lay.mL}x{lay.nL}, "
+                                    f"K={lay.K}, family C2A1C0 fused/DMMA (weak scaling)"),
+                       "baseline_config": cfg, "m": lay.M, "n": lay.N, "k": lay.K, "local_block": [lay.mL, lay.nL],
+                       "grid": [lay.Pr, lay.Pc],
                        "chunks": lay.chunks, "kc": lay.KC, "parallelism": f"2-D C partition {lay.Pr}x{lay.Pc}",
                        "exchange": exchange,
                        "l2_flush": "not needed: per-rank inputs >> 126 MB L2"},
@@ -586,9 +628,18 @@ def bench(args, T, make_plan, world: int, rank: int, local: int) -> int:
                          "peak_source": "FP64 DMMA issue-rate probe run live on each rank's GPU",
                          "note": "per-GPU achieved over the whole step (local GEMMs + exposed exchange)"},
             "exchanged_bytes_per_step_rank0": s.exchanged_bytes / args.steps,
-            "e2e": e2e, "cpu_baseline": None, "clocks": clk.summary(),
+            "verified": verified,
+            "e2e": e2e if e2e_skip is None else {"value": None, "unit": "TFLOP/s", "skipped": e2e_skip},
+            "cpu_baseline": (None if getattr(args, "no_cpu", True) or world > 1 else
+                             B0.cpu_baseline_leg(cfg, "C2A1C0", "f64")),
+            "clocks": clk.summary(),
             "gpu_launches": launches * args.steps,
         }), flush=True)
     dist.barrier()
     dist.destroy_process_group()
+    if verified is not None and not verified["ok"]:
+        import sys
+
+        print(f"PARITY FAILURE: sampled entries outside the bound: {verified}", file=sys.stderr)
+        return 1
     return 0

@@ -39,6 +39,27 @@ def test_bench_line_ours():
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c)
     assert isinstance(d["gpu_launches"], int) and d["gpu_launches"] >= 3
+    v = d["verified"]
+    assert v["ok"] and v["samples"] == 64 and v["steps_accumulated"] == 6 and v["worst_err_over_bound"] <= 1.0
+    # roofline.traffic is set only from an ncu summary of this very build (else null, with the reason)
+    assert d["roofline"]["build_id"]
+    assert d["roofline"]["traffic"] is None or d["roofline"]["traffic_source"]
+
+
+@pytest.mark.parametrize("cfg", ["1", "3a", "3b", "3c", "4", "4tf32"])
+def test_bench_every_baseline_config(cfg):
+    """`--config` runs each BASELINE.json config at its own shape, with the
+    timed run's sampled entries verified against the oracle."""
+    extra = [] if cfg in ("1", "4") else ["--no-e2e"]
+    d = run_bench("--config", cfg, "--steps", "3", "--warmup", "3", "--no-cpu", *extra)
+    assert d["config"]["baseline_config"] == cfg
+    assert d["verified"]["ok"], d["verified"]
+    assert d["value"] > 0 and 0 < d["roofline"]["frac"] <= 1.05
+    if cfg == "1":
+        assert "512 MB" in d["config"]["l2_flush"] and d["config"]["c0"] == "zero"
+        assert d["e2e"]["value"] > 0
+    if cfg.startswith("4"):
+        assert d["dtype"] == ("bf16" if cfg == "4" else "tf32")
 
 
 def test_bench_line_reference_arm():

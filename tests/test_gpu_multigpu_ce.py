@@ -214,7 +214,7 @@ def _bench_worker(rank, world, port, size, q):
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
-        args = argparse.Namespace(size=size, steps=2, warmup=3, no_e2e=False)
+        args = argparse.Namespace(config="5", size=size, steps=2, warmup=3, no_e2e=False, no_verify=False, no_cpu=True)
         out = io.StringIO()
         with contextlib.redirect_stdout(out):
             rc = MG.bench(args, T, bench.make_plan, world, rank, 0)
@@ -227,8 +227,9 @@ def _bench_worker(rank, world, port, size, q):
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_multigpu_bench_arm_world_gt1(world):
-    """The JSON line of the N > 1 bench arm: pulls in both the resident and
-    the e2e step, per-rank work = one size^2 C block (weak scaling)."""
+    """The JSON line of the N > 1 bench arm: config 5 strong-scaled (a fixed
+    size^3 problem over the Pr x Pc grid), pulls in both the resident and the
+    e2e step, and every rank's sampled entries verified against the oracle."""
     import json
 
     if not torch.cuda.is_available():
@@ -236,7 +237,7 @@ def test_multigpu_bench_arm_world_gt1(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, 1024, q)) for r in range(world)]
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, 2048, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=600) for _ in range(world))
@@ -246,7 +247,12 @@ def test_multigpu_bench_arm_world_gt1(world):
         assert tb is None, tb
         assert rc == 0, rank
     line = json.loads(res[0][2].strip().splitlines()[-1])
-    assert line["n_gpus"] == world and line["scaling"] == "weak" and line["value"] > 0
+    assert line["n_gpus"] == world and line["scaling"] == "strong" and line["value"] > 0
+    assert (line["config"]["m"], line["config"]["n"], line["config"]["k"]) == (2048, 2048, 2048)
+    from paper_1904_05717_b200 import multigpu as MG
+
+    assert line["config"]["grid"] == list(MG.grid_shape(world))
+    assert line["verified"]["ok"] and line["verified"]["ranks"] == world
     assert line["config"]["exchange"].startswith("copy-engine pulls")
     assert line["e2e"]["exchange"].startswith("copy-engine pulls") and "events" in line["e2e"]["exchange"]
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0

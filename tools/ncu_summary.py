@@ -3,7 +3,12 @@
 (--metrics gpu__time_duration.sum --csv) into profiles/ncu_summary_<tag>.json.
 
   python tools/ncu_summary.py --rep gpurun_out/prof.ncu-rep --launches gpurun_out/launches.csv \
-      --workload "<bench workload string>" --tag r01 [--flops F] [--model-bytes B]
+      --workload "<bench workload string>" --tag r02_x --launches-per-step 14 [--flops F] [--model-bytes B]
+
+Per-step figures (dram_bytes_per_step, ...) sum the first --launches-per-step
+task-kernel launches of the capture (capture exactly one step's launches);
+the summary is stamped with the library build id, and bench.py only uses its
+bytes when that id equals the loaded library's.
 
 Run here (no GPU needed): ncu -i reads the report offline.
 """
@@ -53,6 +58,11 @@ def main():
     ap.add_argument("--flops", type=float)
     ap.add_argument("--staging", default="cpasync", help="DMMA kernel staging the capture ran with")
     ap.add_argument("--model-bytes", type=float)
+    ap.add_argument("--launches-per-step", type=int, default=1,
+                    help="task-kernel launches in one step of the workload (TMA segments): the first N kernels "
+                         "matching --kernel-regex in the capture are summed into *_per_step")
+    ap.add_argument("--kernel-regex", default=r"k_dmma|k_tc|k_simt", help="which captured kernels are task kernels")
+    ap.add_argument("--build-id", default=None, help="library build id the capture ran (default: the local build)")
     ap.add_argument("--out-dir", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                                       "profiles"))
     a = ap.parse_args()
@@ -81,25 +91,48 @@ def main():
         if "dram_read" in k and "dram_write" in k:
             k["dram_bytes"] = k["dram_read"] + k["dram_write"]
         kernels.append(k)
-    top = kernels[0]
+    import re
+
+    task = [k for k in kernels if re.search(a.kernel_regex, k["kernel"])]
+    if len(task) < a.launches_per_step:
+        raise SystemExit(f"capture holds {len(task)} task-kernel launches, fewer than --launches-per-step "
+                         f"{a.launches_per_step}")
+    step = task[:a.launches_per_step]
+    top = step[0]
+    bid = a.build_id
+    if bid is None:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        from paper_1904_05717_b200 import _native
+
+        bid = _native.build_id()
+    per_step = {
+        "launches_per_step": a.launches_per_step,
+        "dram_bytes_per_step": sum(k.get("dram_bytes", 0.0) for k in step),
+        "duration_s_per_step_under_ncu": sum(k.get("duration", 0.0) for k in step),
+        "l2_read_sectors_from_sm_per_step": sum(k.get("l2_read_sectors_from_sm", 0.0) for k in step),
+    }
     summary = {
         "workload": a.workload,
         "tag": a.tag,
         "staging": a.staging,
         "report": os.path.basename(a.rep),
+        "build_id": bid,
+        **per_step,
         "kernel": top["kernel"],
         "duration_s_under_ncu": top.get("duration"),
-        "dram_bytes_per_launch": top.get("dram_bytes"),
+        "dram_bytes_per_launch": per_step["dram_bytes_per_step"] / a.launches_per_step,
         "tensor_pipe_pct": top.get("tensor_pipe_pct", top.get("tensor_pipe_pct_alt")),
         "kernels": kernels,
         "note": "ncu per-launch times are serialised and cold-cache (clock-control none); compare shares, "
                 "not absolutes, with bench.py's CUDA-event numbers",
     }
-    if a.flops and top.get("duration"):
-        summary["tflops_under_ncu"] = a.flops / top["duration"] / 1e12
-    if a.model_bytes and top.get("dram_bytes"):
+    if a.flops and per_step["duration_s_per_step_under_ncu"]:
+        summary["tflops_under_ncu"] = a.flops / per_step["duration_s_per_step_under_ncu"] / 1e12
+    if a.model_bytes and per_step["dram_bytes_per_step"]:
         summary["model_hbm_bytes"] = a.model_bytes
-        summary["measured_over_model"] = top["dram_bytes"] / a.model_bytes
+        summary["measured_over_model"] = per_step["dram_bytes_per_step"] / a.model_bytes
     if a.launches and os.path.exists(a.launches):
         lines = [ln for ln in open(a.launches) if not ln.startswith("==")]
         rows = list(csv.reader(io.StringIO("".join(lines))))
