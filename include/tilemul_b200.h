@@ -148,6 +148,15 @@ int tm_gpu_hierarchy(int tile, tm_level* levels, int cap, int* count);
 /* build_plan (:90-108): validates and builds the nest; register level must be C. */
 int tm_plan_create(const char* name, const tm_level* levels, int nlevels, int64_t m, int64_t n, int64_t k,
                    const tm_blocksize* bs, int nbs, tm_plan** plan);
+/* A plan straight from an executable LoopNest (plan.hpp:25-31: loops in
+ * nest order, m_r, n_r, shape), for callers that hold a nest but not the
+ * hierarchy it was validated against -- the reference's execute(nest, A, B,
+ * C, opts) (exec.hpp:94-95) takes exactly that. `name` (optional) records the
+ * family member. Checks what execute relies on: extents >= 1, blocksizes
+ * >= 1, cells no larger than the m_r x n_r register tile (exec.hpp:107).
+ * Such a plan executes like any other; it has no I/O model (no hierarchy). */
+int tm_plan_create_loops(const char* name, const tm_loop* loops, int nloops, int64_t m_r, int64_t n_r, int64_t m,
+                         int64_t n, int64_t k, tm_plan** plan);
 void tm_plan_destroy(tm_plan* plan);
 int tm_plan_loops(const tm_plan* plan, tm_loop* loops, int cap, int* count);
 int64_t tm_plan_cells(const tm_plan* plan);

@@ -82,6 +82,7 @@ std::string thrown(const std::function<void()>& f) {
 
 int main() {
     const CacheHierarchy hier = gpu_like();
+    const b200::Options exact{TM_NUMERICS_EXACT};
     // the 3-level members; the level-skipping A2C0 / B2C0 have no feasible derivation with
     // a 128x128 register tile on this hierarchy (blocksizes.hpp:243-425) and are not run
     const std::vector<std::string> members = {"C2A1C0", "B2A1C0", "A2B1C0", "C2B1C0"};
@@ -106,7 +107,7 @@ int main() {
 
             b200::Plan plan(nest, hier);
             MatrixBuffer got = C0;
-            b200::execute(plan, nest, A, B, got, {}, {TM_NUMERICS_EXACT});
+            b200::execute(plan, nest, A, B, got, ExecOptions{}, exact);
             report("exact bitwise " + tag, got.data == want.data);
 
             // prepacked operands in the nest's own layout (plan.hpp:113-124), where the
@@ -122,12 +123,18 @@ int main() {
                 const MatrixBuffer Ap = pack(A, nest), Bp = pack(B, nest);
                 MatrixBuffer wantp = pack(C0, nest), gotp = pack(C0, nest);
                 execute(nest, Ap, Bp, wantp);
-                b200::execute(plan, nest, Ap, Bp, gotp, {}, {TM_NUMERICS_EXACT});
+                b200::execute(plan, nest, Ap, Bp, gotp, ExecOptions{}, exact);
                 report("exact bitwise prepacked " + tag, gotp.data == wantp.data && gotp.layout.blocked());
             }
 
+            // the reference's own call, unchanged: tilemul::execute(nest, A, B, C, opts) (exec.hpp:94-95)
+            // with only the namespace swapped (plan built from the nest's loops, cached per nest)
+            MatrixBuffer same = C0;
+            b200::execute(nest, A, B, same, ExecOptions{}, exact);
+            report("signature-identical exact bitwise " + tag, same.data == want.data);
+
             MatrixBuffer dm = C0;
-            b200::execute(plan, nest, A, B, dm, {}, {TM_NUMERICS_DMMA});
+            b200::execute(nest, A, B, dm);  // default numerics: the DMMA fast path
             double worst = 0;
             const double u = std::ldexp(1.0, -53);
             for (i64 j = 0; j < s.n; ++j)
@@ -157,7 +164,7 @@ int main() {
             const MatrixBuffer Ap = pack(A, nest), Bp = pack(B, nest);
             MatrixBuffer wantp = pack(C0, nest), gotp = pack(C0, nest);
             execute(nest, Ap, Bp, wantp);
-            b200::execute(nest, Ap, Bp, gotp, hier, {}, {TM_NUMERICS_EXACT});
+            b200::execute(nest, Ap, Bp, gotp, hier, ExecOptions{}, exact);
             ++packed_cases;
             report("exact bitwise prepacked C2A1C0 512x512x512", gotp.data == wantp.data && gotp.layout.blocked());
         } catch (const std::invalid_argument& e) {
@@ -173,7 +180,7 @@ int main() {
     MatrixBuffer C = filled(Operand::C, s.m, s.n, rng);
     {  // role mismatch (exec.hpp:67)
         const std::string r = thrown<std::invalid_argument>([&] { execute(nest, B, B, C); });
-        const std::string g = thrown<std::invalid_argument>([&] { b200::execute(nest, B, B, C, hier); });
+        const std::string g = thrown<std::invalid_argument>([&] { b200::execute(nest, B, B, C); });
         report("role mismatch -> invalid_argument", r == g && r.rfind("WRONG", 0) != 0 && r != "NO THROW", g);
     }
     {  // parallel loop along k (exec.hpp:127-131)
@@ -184,7 +191,7 @@ int main() {
         eo.workers = 2;
         eo.parallel_loop = kl;
         const std::string r = thrown<std::invalid_argument>([&] { execute(nest, A, B, C, eo); });
-        const std::string g = thrown<std::invalid_argument>([&] { b200::execute(nest, A, B, C, hier, eo); });
+        const std::string g = thrown<std::invalid_argument>([&] { b200::execute(nest, A, B, C, eo); });
         report("k-parallel -> invalid_argument", r == g && r.rfind("WRONG", 0) != 0 && r != "NO THROW", g);
     }
     {  // blocksizes that break the fit rules: ValidationFailure, same rule ids in order (blocksizes.hpp:125-235)
@@ -207,6 +214,32 @@ int main() {
         for (const auto& x : got) ids += x + " ";
         report("bad blocksizes -> ValidationFailure with the reference's rules",
                what == "ValidationFailure" && !ref.empty() && got == ref, ids);
+    }
+    {  // a plan used with another nest (advisor r01): invalid_argument, never a silent out-of-bounds run
+        const LoopNest other = plan_for("C2A1C0", Shape(256, 384, 520), hier);
+        b200::Plan p(nest);
+        MatrixBuffer Co = filled(Operand::C, 256, 384, rng);
+        const MatrixBuffer Ao = filled(Operand::A, 256, 520, rng), Bo = filled(Operand::B, 520, 384, rng);
+        const std::string g = thrown<std::invalid_argument>([&] { b200::execute(p, other, Ao, Bo, Co); });
+        report("plan/nest mismatch -> invalid_argument", g.rfind("WRONG", 0) != 0 && g != "NO THROW", g);
+    }
+    {  // a nest assembled by hand (no build_plan, no descriptor): executed from its loops alone
+        LoopNest hand;
+        hand.shape = Shape(130, 70, 90);
+        hand.loops = {NestStep{1, Dim::k, 32, false}, NestStep{1, Dim::n, 40, false}, NestStep{0, Dim::n, 20, false},
+                      NestStep{0, Dim::m, 64, false}};
+        hand.m_r = 64;
+        hand.n_r = 20;
+        const MatrixBuffer Ah = filled(Operand::A, 130, 90, rng), Bh = filled(Operand::B, 90, 70, rng);
+        const MatrixBuffer Ch = filled(Operand::C, 130, 70, rng);
+        MatrixBuffer want = Ch, got = Ch;
+        execute(hand, Ah, Bh, want);
+        b200::execute(hand, Ah, Bh, got, ExecOptions{}, exact);
+        report("hand-built nest exact bitwise", got.data == want.data);
+        LoopNest wide = hand;
+        wide.m_r = 32;  // cells of 64 rows exceed the register tile the reference's scratch holds (exec.hpp:107)
+        const std::string g = thrown<std::invalid_argument>([&] { b200::execute(wide, Ah, Bh, got); });
+        report("cells larger than m_r x n_r -> invalid_argument", g.rfind("WRONG", 0) != 0 && g != "NO THROW", g);
     }
     std::printf("{\"summary\": true, \"failures\": %d}\n", g_fail);
     return g_fail == 0 ? 0 : 1;

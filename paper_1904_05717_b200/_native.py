@@ -69,6 +69,7 @@ SIGNATURES = [
     ("tm_gpu_hierarchy", C.c_int, [C.c_int, C.POINTER(tm_level), C.c_int, C.POINTER(C.c_int)]),
     ("tm_plan_create", C.c_int, [cstr, C.POINTER(tm_level), C.c_int, i64, i64, i64, C.POINTER(tm_blocksize), C.c_int,
                                  C.POINTER(P)]),
+    ("tm_plan_create_loops", C.c_int, [cstr, C.POINTER(tm_loop), C.c_int, i64, i64, i64, i64, i64, C.POINTER(P)]),
     ("tm_plan_destroy", None, [P]),
     ("tm_plan_loops", C.c_int, [P, C.POINTER(tm_loop), C.c_int, C.POINTER(C.c_int)]),
     ("tm_plan_cells", i64, [P]),

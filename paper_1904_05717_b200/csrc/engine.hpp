@@ -106,6 +106,14 @@ struct tm_plan {
     std::map<mmm::engine::Key, std::unique_ptr<mmm::engine::Schedule>> schedules;
     std::mutex mu;
     std::mutex host_mu;  // one tm_execute_host at a time per plan (it owns the plan's staging buffers and streams)
+    // device-operand launches share the schedules' scratch (task lists,
+    // progress / fix-up counters, split-k slots): each launch's stream waits
+    // for the previous launch of this plan (on any stream) to finish with it
+    cudaEvent_t order = nullptr;
+    // tm_execute_packed's column-major scratch, ordered across streams by packed_done
+    std::mutex packed_mu;
+    double *pA = nullptr, *pB = nullptr, *pC = nullptr;
+    cudaEvent_t packed_done = nullptr;
     // host-buffer execution
     double *dA = nullptr, *dB = nullptr, *dC = nullptr;
     cudaStream_t host_stream = nullptr, copy_stream = nullptr, d2h_stream = nullptr;
@@ -121,6 +129,11 @@ struct tm_plan {
         if (dA) cudaFree(dA);
         if (dB) cudaFree(dB);
         if (dC) cudaFree(dC);
+        if (pA) cudaFree(pA);
+        if (pB) cudaFree(pB);
+        if (pC) cudaFree(pC);
+        if (order) cudaEventDestroy(order);
+        if (packed_done) cudaEventDestroy(packed_done);
         for (auto ev : chunk_ready) cudaEventDestroy(ev);
         if (host_stream) cudaStreamDestroy(host_stream);
         if (copy_stream) cudaStreamDestroy(copy_stream);

@@ -553,6 +553,9 @@ void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t l
     Schedule& s = *slot;
     const bool vec16 = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(B) % 16 == 0) && origins_even(s.host_tasks);
+    // this plan's previous launch (any stream) is done with the shared scratch before this one starts
+    if (!plan->order) cuda_check(cudaEventCreateWithFlags(&plan->order, cudaEventDisableTiming), "order event");
+    else cuda_check(cudaStreamWaitEvent(stream, plan->order, 0), "order after the previous launch");
     if (s.regions > 0)
         cuda_check(cudaMemsetAsync(s.progress, 0, sizeof(int32_t) * static_cast<std::size_t>(s.regions), stream),
                    "reset progress");
@@ -565,6 +568,7 @@ void run(tm_plan* plan, const double* A, int64_t lda, const double* B, int64_t l
                    "split-k reduce launch");
         ++launches;
     }
+    cuda_check(cudaEventRecord(plan->order, stream), "record launch order");
     plan->last_tasks = static_cast<int64_t>(s.host_tasks.size());
     plan->last_launches = launches;
     plan->last_ctas = s.grid;

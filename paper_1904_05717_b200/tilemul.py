@@ -539,6 +539,29 @@ class LoopNest:  # plan.hpp:25-85
         self.m_r = bs.get(0, "m")
         self.n_r = bs.get(0, "n")
 
+    @classmethod
+    def from_loops(cls, loops: Sequence[NestStep], m_r: int, n_r: int, shape: Shape,
+                   name: Optional[str] = None) -> "LoopNest":
+        """An executable nest from its loop list alone (plan.hpp:25-31), the
+        way the reference's execute(nest, A, B, C, opts) receives it: no
+        hierarchy (so no model()); tm_plan_create_loops checks what execution
+        relies on."""
+        self = cls.__new__(cls)
+        arr = (N.tm_loop * max(1, len(loops)))()
+        for i, L in enumerate(loops):
+            arr[i] = N.tm_loop(L.level, L.dim.encode(), L.blocksize, 1 if L.cap else 0)
+        ptr = C.c_void_p(None)
+        _check(N.lib().tm_plan_create_loops(name.encode() if name else None, arr, len(loops), m_r, n_r, shape.m,
+                                            shape.n, shape.k, C.byref(ptr)))
+        self._ptr = ptr
+        self.shape = shape
+        self.descriptor = parse_name(name) if name else None
+        self.blocksizes = None
+        self.hierarchy = None
+        self.loops = list(loops)
+        self.m_r, self.n_r = m_r, n_r
+        return self
+
     def __del__(self):
         p = getattr(self, "_ptr", None)
         if p is not None and p.value and N is not None and N._lib is not None:
@@ -887,6 +910,29 @@ class LruSimulator:  # cachesim.hpp:61-354
                                      int(o.flush_dirty_at_end), C.byref(ptr)))
         self._ptr = ptr
         self._nlev = hier.size() - (0 if o.include_registers else 1)
+
+    @classmethod
+    def from_loops(cls, loops: Sequence[NestStep], m_r: int, n_r: int, shape: Shape,
+                   name: Optional[str] = None) -> "LoopNest":
+        """An executable nest from its loop list alone (plan.hpp:25-31), the
+        way the reference's execute(nest, A, B, C, opts) receives it: no
+        hierarchy (so no model()); tm_plan_create_loops checks what execution
+        relies on."""
+        self = cls.__new__(cls)
+        arr = (N.tm_loop * max(1, len(loops)))()
+        for i, L in enumerate(loops):
+            arr[i] = N.tm_loop(L.level, L.dim.encode(), L.blocksize, 1 if L.cap else 0)
+        ptr = C.c_void_p(None)
+        _check(N.lib().tm_plan_create_loops(name.encode() if name else None, arr, len(loops), m_r, n_r, shape.m,
+                                            shape.n, shape.k, C.byref(ptr)))
+        self._ptr = ptr
+        self.shape = shape
+        self.descriptor = parse_name(name) if name else None
+        self.blocksizes = None
+        self.hierarchy = None
+        self.loops = list(loops)
+        self.m_r, self.n_r = m_r, n_r
+        return self
 
     def __del__(self):
         p = getattr(self, "_ptr", None)

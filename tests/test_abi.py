@@ -82,3 +82,25 @@ def test_cpp_shim_compiles_against_the_reference():
     finally:
         os.unlink(f.name)
     assert r.returncode == 0 and "warning" not in r.stderr, r.stderr
+
+
+def test_plan_from_loops_checks_and_has_no_model():
+    """tm_plan_create_loops (the signature-identical drop-in's plan): cells
+    larger than the register tile are a usage error; such a plan has no
+    hierarchy, so no model; a valid one walks the given loops."""
+    steps = [T.NestStep(1, "k", 32), T.NestStep(1, "n", 40), T.NestStep(0, "n", 20), T.NestStep(0, "m", 64)]
+    nest = T.LoopNest.from_loops(steps, 64, 20, T.Shape(130, 70, 90), name=None)
+    assert nest.cell_count() == 3 * 2 * 2 * 3 and nest.loops == steps
+    with pytest.raises(ValueError):
+        nest.model()
+    with pytest.raises(ValueError):
+        T.LoopNest.from_loops(steps, 32, 20, T.Shape(130, 70, 90))  # 64-row cells > m_r = 32
+    named = T.LoopNest.from_loops(steps, 64, 20, T.Shape(130, 70, 90), name="B1C0")
+    assert T.format_name(named.descriptor) == "B1C0"
+
+
+def test_build_id_matches_sources():
+    from paper_1904_05717_b200 import build as B
+
+    assert N.build_id() == B.source_hash()
+    assert N.build_id() in N.lib().tm_version().decode()

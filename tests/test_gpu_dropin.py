@@ -31,4 +31,5 @@ def test_reference_api_with_b200_execute():
     assert summary and summary[0]["failures"] == 0, (r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0, r.stderr[-2000:]
     kinds = {x["check"].split(" ")[0] for x in lines if "check" in x}
-    assert {"exact", "dmma", "role", "k-parallel", "bad"} <= kinds
+    assert {"exact", "dmma", "role", "k-parallel", "bad", "signature-identical", "plan/nest", "hand-built",
+            "cells"} <= kinds
