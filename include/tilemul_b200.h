@@ -279,6 +279,19 @@ int tm_sim_finish(tm_sim* sim, tm_sim_level* out, int cap, int* count, int64_t* 
 /* Lines resident at one simulated level (position innermost first), in slot order (:174-182). */
 int tm_sim_resident_lines(const tm_sim* sim, int position, int64_t* lines, int cap, int* count);
 
+/* --- multi-GPU exchange (no reference counterpart: the
+ * reference is single-node shared memory, exec.hpp:121-137) -------------- */
+/* Export the CUDA IPC handle (64 bytes into `handle`) of the device
+ * allocation holding `ptr`, and ptr's byte offset inside it. */
+int tm_ipc_export(const void* ptr, void* handle, int64_t* offset);
+/* Map a peer process's allocation on the CURRENT device (lazy peer access);
+ * *ptr = its base + offset. */
+int tm_ipc_open(const void* handle, int64_t offset, void** ptr);
+int tm_ipc_close(void* ptr, int64_t offset);
+/* Device-to-device copy on `stream` by the copy engines (peer memory over
+ * NVLink when src is a mapped peer allocation). */
+int tm_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -71,6 +71,10 @@ SIGNATURES = [
                                  C.POINTER(P)]),
     ("tm_plan_create_loops", C.c_int, [cstr, C.POINTER(tm_loop), C.c_int, i64, i64, i64, i64, i64, C.POINTER(P)]),
     ("tm_plan_destroy", None, [P]),
+    ("tm_ipc_export", C.c_int, [P, P, C.POINTER(i64)]),
+    ("tm_ipc_open", C.c_int, [P, i64, C.POINTER(P)]),
+    ("tm_ipc_close", C.c_int, [P, i64]),
+    ("tm_copy_async", C.c_int, [P, P, i64, P]),
     ("tm_plan_loops", C.c_int, [P, C.POINTER(tm_loop), C.c_int, C.POINTER(C.c_int)]),
     ("tm_plan_cells", i64, [P]),
     ("tm_plan_model", C.c_int, [P, C.POINTER(i64), C.c_int]),

@@ -90,6 +90,26 @@ int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t 
 // `tma`: the operands allow TMA staging (16-byte aligned bases and leading
 // dimensions, staging not forced to cp.async).
 gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o, bool tma);
+// The host half of the lowering (no device calls): the task list of the
+// nest for a kernel with tile_m x tile_n tiles on a machine with `slots`
+// resident CTAs, plus what the device half allocates for it. Also the input
+// of the GPU-mode I/O model (gpu_model.cpp), which runs without a GPU.
+struct HostSchedule {
+    std::vector<gpu::Task> tasks;
+    bool blocked = false;            // stream-K: CTA c runs tasks first[c] .. first[c+1]-1
+    int grid_fixed = 0;
+    std::vector<int32_t> first;
+    bool fixup = false;              // split tiles finished in-kernel (Task::fixup)
+    int32_t slots = 0;               // split-k workspace slots
+    int32_t counters = 0;            // fix-up counters
+    std::vector<gpu::ReduceTile> red;  // tiles summed by the reduce launch (kernels without the fix-up)
+    int regions = 0;                 // faithful: per-region progress counters
+};
+HostSchedule plan_tasks(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, int tile_m, int tile_n,
+                        int slots);
+// Tile shape and occupancy of a kernel: measured on the device (query) or
+// the compiled-in values (the model's CPU path).
+gpu::KernelInfo kernel_tiles(gpu::Kernel kernel, bool query);
 // Lowers the nest onto CTA tasks for `kernel` (schedule, split and fix-up
 // per opts). upload = false builds the host task list only.
 std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, cudaStream_t stream,

@@ -109,27 +109,17 @@ gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o, bool tma) {
 
 // Splits one C region into kernel tiles, n outer / m inner (the register
 // plan's own loop order, C0 = n then m).
-std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, cudaStream_t stream,
-                                bool upload) {
-    auto s = std::make_unique<Schedule>();
-    s->kernel = kernel;
-    gpu::KernelInfo info{};
-    const bool wide = kernel == gpu::kTc2wBf16 || kernel == gpu::kTc2wTf32;
-    const bool pair = kernel == gpu::kTc2Bf16 || kernel == gpu::kTc2Tf32 || wide;
-    if (kernel == gpu::kTcBf16 || kernel == gpu::kTcTf32)
-        info = gpu::KernelInfo{128, 256, 256, gpu::tc_smem_bytes(kernel == gpu::kTcTf32), 1};
-    else if (wide)
-        info = gpu::KernelInfo{256, 512, 384, gpu::tc2_smem_bytes(kernel == gpu::kTc2wTf32, true), 1};
-    else if (pair)
-        info = gpu::KernelInfo{256, 256, 256, gpu::tc2_smem_bytes(kernel == gpu::kTc2Tf32), 1};
-    else
-        cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
-    const int slots = sm_count() * std::max(1, info.ctas_per_sm);
+HostSchedule plan_tasks(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, int tile_m, int tile_n,
+                        int slots) {
+    HostSchedule hs;
+    struct {
+        int tile_m, tile_n;
+    } info{tile_m, tile_n};
     const Extents& e = nest.ext;
     check_i32(e.m, "m");
     check_i32(e.n, "n");
     check_i32(e.k, "k");
-    auto& T = s->host_tasks;
+    auto& T = hs.tasks;
 
     if (o.schedule == TM_SCHEDULE_FUSED) {
         // First-appearance order of the register-level C blocks = the walk of
@@ -227,26 +217,13 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
                 }
             }
             first[static_cast<std::size_t>(G)] = static_cast<int32_t>(T.size());
-            s->blocked = true;
-            s->grid_fixed = G;
-            cuda_check(cudaMalloc(&s->cta_first, sizeof(int32_t) * first.size()), "cudaMalloc(cta ranges)");
-            cuda_check(cudaMemcpyAsync(s->cta_first, first.data(), sizeof(int32_t) * first.size(),
-                                       cudaMemcpyHostToDevice, stream),
-                       "upload cta ranges");
-            if (fixk) {
-                alloc_fixup(*s, info, next_slot, ncounters, stream);
-            } else if (!red.empty()) {
-                s->slices = static_cast<int>(red.size());
-                s->work_ld = info.tile_m;
-                s->work_slice = static_cast<i64>(info.tile_m) * info.tile_n;
-                cuda_check(cudaMalloc(&s->work, sizeof(double) * static_cast<std::size_t>(s->work_slice) * next_slot),
-                           "cudaMalloc(stream-k workspace)");
-                cuda_check(cudaMalloc(&s->reduce, sizeof(gpu::ReduceTile) * red.size()), "cudaMalloc(reduce list)");
-                cuda_check(cudaMemcpyAsync(s->reduce, red.data(), sizeof(gpu::ReduceTile) * red.size(),
-                                           cudaMemcpyHostToDevice, stream),
-                           "upload reduce list");
-            }
-            cuda_check(cudaStreamSynchronize(stream), "upload stream-k lists (sync)");
+            hs.blocked = true;
+            hs.grid_fixed = G;
+            hs.first = std::move(first);
+            hs.fixup = fixk;
+            hs.slots = next_slot;
+            hs.counters = fixk ? ncounters : 0;
+            if (!fixk) hs.red = std::move(red);
         } else {
         // k parts per tile. split_k > 1: every tile; split_k == 0 (auto):
         // every tile when C has too few tiles to fill the machine, otherwise
@@ -337,19 +314,10 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
             }
             next_slot += used;
         }
-        if (fix) alloc_fixup(*s, info, next_slot, ncounters, stream);
-        s->slices = static_cast<int>(red.size());
-        if (!red.empty()) {
-            s->work_ld = info.tile_m;
-            s->work_slice = static_cast<i64>(info.tile_m) * info.tile_n;
-            cuda_check(cudaMalloc(&s->work, sizeof(double) * static_cast<std::size_t>(s->work_slice) * next_slot),
-                       "cudaMalloc(split-k workspace)");
-            cuda_check(cudaMalloc(&s->reduce, sizeof(gpu::ReduceTile) * red.size()), "cudaMalloc(reduce list)");
-            cuda_check(cudaMemcpyAsync(s->reduce, red.data(), sizeof(gpu::ReduceTile) * red.size(),
-                                       cudaMemcpyHostToDevice, stream),
-                       "upload reduce list");
-            cuda_check(cudaStreamSynchronize(stream), "upload reduce list (sync)");
-        }
+        hs.fixup = fix;
+        hs.slots = next_slot;
+        hs.counters = fix ? ncounters : 0;
+        hs.red = std::move(red);
         }  // uniform / tail split
     } else if (o.schedule == TM_SCHEDULE_FAITHFUL) {
         const i64 cells = nest.cells();
@@ -406,14 +374,72 @@ std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Ke
                 order.emplace_back((static_cast<double>(r) + 0.5) / static_cast<double>(workers[w].size()), w, r);
         std::sort(order.begin(), order.end());
         for (const auto& [key, w, r] : order) T.push_back(workers[w][r]);
-        s->regions = static_cast<int>(regions.size());
-        cuda_check(cudaMalloc(&s->progress, sizeof(int32_t) * static_cast<std::size_t>(std::max(1, s->regions))),
-                   "cudaMalloc(progress)");
+        hs.regions = static_cast<int>(regions.size());
     } else {
         fail_usage("unknown schedule");
     }
     if (T.size() > static_cast<std::size_t>(INT32_MAX)) fail_usage("too many tasks");
+    return hs;
+}
+
+gpu::KernelInfo kernel_tiles(gpu::Kernel kernel, bool query) {
+    const bool wide = kernel == gpu::kTc2wBf16 || kernel == gpu::kTc2wTf32;
+    const bool pair = kernel == gpu::kTc2Bf16 || kernel == gpu::kTc2Tf32 || wide;
+    if (kernel == gpu::kTcBf16 || kernel == gpu::kTcTf32)
+        return gpu::KernelInfo{128, 256, 256, query ? gpu::tc_smem_bytes(kernel == gpu::kTcTf32) : 0, 1};
+    if (wide) return gpu::KernelInfo{256, 512, 384, query ? gpu::tc2_smem_bytes(kernel == gpu::kTc2wTf32, true) : 0, 1};
+    if (pair) return gpu::KernelInfo{256, 256, 256, query ? gpu::tc2_smem_bytes(kernel == gpu::kTc2Tf32) : 0, 1};
+    if (query) {
+        gpu::KernelInfo info{};
+        cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
+        return info;
+    }
+    // the DMMA / SIMT tiles and their occupancy (gpu::kernel_info measures it on a device)
+    switch (kernel) {
+        case gpu::kDmma128: return gpu::KernelInfo{128, 128, 512, 0, 1};
+        case gpu::kDmma128x64: return gpu::KernelInfo{128, 64, 128, 0, 2};
+        case gpu::kFma128: return gpu::KernelInfo{128, 128, 256, 0, 1};
+        default: return gpu::KernelInfo{64, 64, 128, 0, 1};
+    }
+}
+
+std::unique_ptr<Schedule> lower(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, cudaStream_t stream,
+                                bool upload) {
+    auto s = std::make_unique<Schedule>();
+    s->kernel = kernel;
+    const gpu::KernelInfo info = kernel_tiles(kernel, true);
+    const bool wide = kernel == gpu::kTc2wBf16 || kernel == gpu::kTc2wTf32;
+    const bool pair = kernel == gpu::kTc2Bf16 || kernel == gpu::kTc2Tf32 || wide;
+    const int slots = sm_count() * std::max(1, info.ctas_per_sm);
+    HostSchedule hs = plan_tasks(nest, o, kernel, info.tile_m, info.tile_n, slots);
+    s->host_tasks = std::move(hs.tasks);
+    auto& T = s->host_tasks;
     if (!upload) return s;  // host task list only (callers that splice task lists)
+    if (hs.blocked) {
+        s->blocked = true;
+        s->grid_fixed = hs.grid_fixed;
+        cuda_check(cudaMalloc(&s->cta_first, sizeof(int32_t) * hs.first.size()), "cudaMalloc(cta ranges)");
+        cuda_check(cudaMemcpyAsync(s->cta_first, hs.first.data(), sizeof(int32_t) * hs.first.size(),
+                                   cudaMemcpyHostToDevice, stream),
+                   "upload cta ranges");
+    }
+    if (hs.fixup) alloc_fixup(*s, info, hs.slots, hs.counters, stream);
+    if (!hs.red.empty()) {
+        s->slices = static_cast<int>(hs.red.size());
+        s->work_ld = info.tile_m;
+        s->work_slice = static_cast<i64>(info.tile_m) * info.tile_n;
+        cuda_check(cudaMalloc(&s->work, sizeof(double) * static_cast<std::size_t>(s->work_slice) * hs.slots),
+                   "cudaMalloc(split-k workspace)");
+        cuda_check(cudaMalloc(&s->reduce, sizeof(gpu::ReduceTile) * hs.red.size()), "cudaMalloc(reduce list)");
+        cuda_check(cudaMemcpyAsync(s->reduce, hs.red.data(), sizeof(gpu::ReduceTile) * hs.red.size(),
+                                   cudaMemcpyHostToDevice, stream),
+                   "upload reduce list");
+    }
+    if (hs.regions > 0) {
+        s->regions = hs.regions;
+        cuda_check(cudaMalloc(&s->progress, sizeof(int32_t) * static_cast<std::size_t>(s->regions)),
+                   "cudaMalloc(progress)");
+    }
     // Persistent grid: every CTA must be co-resident for the faithful
     // schedule's waits to make progress.
     int grid = o.ctas > 0 ? std::min(o.ctas, slots) : slots;

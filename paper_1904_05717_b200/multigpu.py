@@ -125,44 +125,52 @@ class Summa:
 
     def attach_peers(self, A_local, B_local) -> bool:
         """Copy-engine exchange: map every row peer's A pieces and column
-        peer's B pieces (CUDA IPC; all ranks must call, after filling their
-        pieces). The pieces must stay unchanged while peers read them.
-        Collective and all-or-nothing: returns whether every rank mapped its
-        peers; if any could not, no rank pulls (the broadcasts stay in use)."""
+        peer's B pieces (CUDA IPC handles exported and opened by the native
+        library on each rank's own device, lazy peer access; all ranks must
+        call, after filling their pieces). The pieces must stay unchanged
+        while peers read them. Collective and all-or-nothing: returns whether
+        every rank mapped its peers; if any could not, no rank pulls (the
+        broadcasts stay in use)."""
         import torch
+
+        from . import tilemul as T
 
         lay = self.lay
         mine, err = None, None
         try:
-            from torch.multiprocessing.reductions import reduce_tensor
-
-            mine = (reduce_tensor(A_local), reduce_tensor(B_local))
+            mine = (T.ipc_export(A_local), T.ipc_export(B_local))
         except Exception as exc:  # noqa: BLE001 -- e.g. allocations IPC cannot export
             err = exc
         allh = [None] * (lay.Pr * lay.Pc)
         self.dist.all_gather_object(allh, mine)
-        peer_a, peer_b = {}, {}
+        peer_a, peer_b, opened = {}, {}, []
         if err is None and all(h is not None for h in allh):
             try:
-                for c in range(lay.Pc):
-                    if c != self.c:
-                        fn, args = allh[lay.rank_of(self.r, c)][0]
-                        peer_a[c] = fn(*args)
-                for r in range(lay.Pr):
-                    if r != self.r:
-                        fn, args = allh[lay.rank_of(r, self.c)][1]
-                        peer_b[r] = fn(*args)
+                with torch.cuda.device(self.device):
+                    for c in range(lay.Pc):
+                        if c != self.c:
+                            h, off = allh[lay.rank_of(self.r, c)][0]
+                            peer_a[c] = T.ipc_open(h, off)
+                            opened.append((peer_a[c], off))
+                    for r in range(lay.Pr):
+                        if r != self.r:
+                            h, off = allh[lay.rank_of(r, self.c)][1]
+                            peer_b[r] = T.ipc_open(h, off)
+                            opened.append((peer_b[r], off))
             except Exception as exc:  # noqa: BLE001
                 err = exc
         else:
             err = err or RuntimeError("a peer could not export its pieces")
-        ok = [err is None]
         oks = [None] * (lay.Pr * lay.Pc)
-        self.dist.all_gather_object(oks, ok)  # every rank maps its peers before any rank relies on it
-        if not all(o[0] for o in oks):
+        self.dist.all_gather_object(oks, err is None)  # every rank maps its peers before any rank relies on it
+        if not all(oks):
+            for ptr, off in opened:
+                T.ipc_close(ptr, off)
             self.peer_a = self.peer_b = None
+            self.attach_error = repr(err) if err is not None else "a peer failed to map"
             return False
         self.peer_a, self.peer_b = peer_a, peer_b
+        self._opened = opened
         self.ce_stream = torch.cuda.Stream(device=self.device)
         return True
 
@@ -244,7 +252,17 @@ class Summa:
 
     def detach_peers(self) -> None:
         """Back to the broadcasts (collective: call on every rank)."""
+        import torch
+
+        from . import tilemul as T
+
+        if self.ce_stream is not None:
+            self.ce_stream.synchronize()
         self.dist.barrier()  # no rank still pulls from a peer whose pieces are about to change
+        with torch.cuda.device(self.device):
+            for ptr, off in getattr(self, "_opened", []):
+                T.ipc_close(ptr, off)
+        self._opened = []
         self.peer_a = self.peer_b = None
         self.step_sync = False
 
@@ -271,16 +289,22 @@ class Summa:
             return a, b, []
         st = self.ce_stream
         st.wait_stream(torch.cuda.current_stream(self.device))  # the buffer's last reader (GEMM j-2) is queued there
+        from . import tilemul as T
+
         with torch.cuda.stream(st):
+            # one cudaMemcpyAsync per chunk piece, on the side stream, from the peer's mapped
+            # allocation (copy engines over NVLink; no SM, no second context on the peer's device)
             if a_src_c != self.c:
                 if self.step_sync:
                     st.wait_event(self.peer_up_a[j])
-                a.copy_(self.a_chunk_view(self.peer_a[a_src_c], j), non_blocking=True)
+                src = self.peer_a[a_src_c] + 8 * lay.a_local_chunk(j) * lay.mL * lay.KC
+                T.copy_async(a.data_ptr(), src, a.numel() * 8, st)
                 self.exchanged_bytes += a.numel() * 8
             if b_src_r != self.r:
                 if self.step_sync:
                     st.wait_event(self.peer_up_b[j])
-                b.copy_(self.b_chunk_view(self.peer_b[b_src_r], j), non_blocking=True)
+                src = self.peer_b[b_src_r] + 8 * lay.b_local_chunk(j) * lay.KC * lay.nL
+                T.copy_async(b.data_ptr(), src, b.numel() * 8, st)
                 self.exchanged_bytes += b.numel() * 8
             if self.step_sync:
                 self.got[j].record(st)

@@ -774,6 +774,36 @@ def fill_uniform_block(x, rows: int, cols: int, ld: int, seed: int, row0: int, c
     _check(N.lib().tm_fill_uniform_block(x.data_ptr(), rows, cols, ld, seed, row0, col0, global_ld, C.c_void_p(st)))
 
 
+# ------------------------------------------ multi-GPU exchange (copy engines)
+def ipc_export(x) -> Tuple[bytes, int]:
+    """(CUDA IPC handle of the allocation holding CUDA tensor x, x's byte
+    offset in it) -- for a peer process to map with ipc_open."""
+    h = (C.c_ubyte * 64)()
+    off = C.c_int64(0)
+    _check(N.lib().tm_ipc_export(C.c_void_p(x.data_ptr()), h, C.byref(off)))
+    return bytes(h), off.value
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    """Map a peer's exported allocation on the current device; returns the
+    device address of the exported tensor's first byte."""
+    h = (C.c_ubyte * 64).from_buffer_copy(handle)
+    p = C.c_void_p(None)
+    _check(N.lib().tm_ipc_open(h, offset, C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int, offset: int) -> None:
+    _check(N.lib().tm_ipc_close(C.c_void_p(ptr), offset))
+
+
+def copy_async(dst: int, src: int, nbytes: int, stream) -> None:
+    """Device-to-device copy by the copy engines on `stream` (a
+    torch.cuda.Stream or raw handle); src may be a mapped peer address."""
+    st = getattr(stream, "cuda_stream", stream)
+    _check(N.lib().tm_copy_async(C.c_void_p(dst), C.c_void_p(src), nbytes, C.c_void_p(st)))
+
+
 def measure_tc_peak(dtype: str = "bf16", launches: int = 10, sustained: bool = False) -> float:
     """Peak tcgen05 MMA TFLOP/s of the current device for bf16 or tf32 inputs
     (roofline denominator): ~5 ms bursts at full clocks, or ~200 ms launches
@@ -910,29 +940,6 @@ class LruSimulator:  # cachesim.hpp:61-354
                                      int(o.flush_dirty_at_end), C.byref(ptr)))
         self._ptr = ptr
         self._nlev = hier.size() - (0 if o.include_registers else 1)
-
-    @classmethod
-    def from_loops(cls, loops: Sequence[NestStep], m_r: int, n_r: int, shape: Shape,
-                   name: Optional[str] = None) -> "LoopNest":
-        """An executable nest from its loop list alone (plan.hpp:25-31), the
-        way the reference's execute(nest, A, B, C, opts) receives it: no
-        hierarchy (so no model()); tm_plan_create_loops checks what execution
-        relies on."""
-        self = cls.__new__(cls)
-        arr = (N.tm_loop * max(1, len(loops)))()
-        for i, L in enumerate(loops):
-            arr[i] = N.tm_loop(L.level, L.dim.encode(), L.blocksize, 1 if L.cap else 0)
-        ptr = C.c_void_p(None)
-        _check(N.lib().tm_plan_create_loops(name.encode() if name else None, arr, len(loops), m_r, n_r, shape.m,
-                                            shape.n, shape.k, C.byref(ptr)))
-        self._ptr = ptr
-        self.shape = shape
-        self.descriptor = parse_name(name) if name else None
-        self.blocksizes = None
-        self.hierarchy = None
-        self.loops = list(loops)
-        self.m_r, self.n_r = m_r, n_r
-        return self
 
     def __del__(self):
         p = getattr(self, "_ptr", None)

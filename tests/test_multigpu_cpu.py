@@ -77,8 +77,9 @@ def _worker(rank, world, port, mL, nL, K, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_summa_gloo(world):
+    """World 8 is the 2 x 4 grid the 8-GPU config-5 run uses."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -104,3 +105,21 @@ def test_layout_and_ownership():
     assert [lay.b_owner(j) for j in range(8)] == [0, 0, 0, 0, 1, 1, 1, 1]
     with pytest.raises(ValueError):
         MG.make_layout(8, 16, 16, 12)
+
+
+def test_config5_layouts_fit_one_b200():
+    """BASELINE config 5 (65536^3, strong scaled) at N = 1, 2, 4, 8: the grid,
+    chunking and each rank's resident bytes (pieces + receive buffers) fit in
+    a B200's 180 GB; the exchanged volume per step is what a rank does not own
+    of its A row panel and B column panel (SURVEY.md §8e volumes)."""
+    S = 65536
+    want_grid = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
+    for P, (pr, pc) in want_grid.items():
+        lay = MG.make_layout(P, S // pr, S // pc, S)
+        assert (lay.Pr, lay.Pc, lay.M, lay.N, lay.K) == (pr, pc, S, S, S)
+        resident = 8 * (lay.mL * lay.K // lay.Pc + lay.K // lay.Pr * lay.nL + lay.mL * lay.nL)
+        recv = 8 * (2 * lay.mL * lay.KC * (lay.Pc > 1) + 2 * lay.KC * lay.nL * (lay.Pr > 1))
+        assert resident + recv < 170e9, (P, resident, recv)
+        exchanged = 8 * (lay.mL * lay.K * (lay.Pc - 1) // lay.Pc + lay.nL * lay.K * (lay.Pr - 1) // lay.Pr)
+        if P == 8:  # A 12.9 GB + B 4.3 GB per rank (SURVEY.md §8e)
+            assert abs(exchanged - 17.18e9) < 0.01e9

@@ -44,8 +44,16 @@ UNIT = {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0, "byte": 1, "Kbyte": 1e3, "
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True)
-    rows = list(csv.reader(io.StringIO(out.stdout)))
+    """Header, units and rows of an ncu --page raw --csv export: read from a
+    .csv made on the GPU box (`ncu -i X.ncu-rep --page raw --csv > X.csv`; a
+    full-set report of many launches is too large to bring back) or exported
+    here from a .ncu-rep."""
+    if rep.endswith(".csv"):
+        text = "".join(ln for ln in open(rep) if not ln.startswith("=="))
+    else:
+        text = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                              check=True).stdout
+    rows = list(csv.reader(io.StringIO(text)))
     return rows[0], rows[1], rows[2:]
 
 
