@@ -247,14 +247,15 @@ class ClockSampler:
                 "power_w_median": statistics.median(power) if power else None}
 
 
-def ncu_traffic(workload, staging, launches_per_step):
+def ncu_traffic(workload, staging, launches_per_step, blocksizes=None):
     """DRAM bytes per launch (and per step) of the task kernel from the
     committed ncu --set full summary of this workload and staging -- only if
-    that summary was captured from THIS build (its build id equals the loaded
-    library's) with the same launches per step. Otherwise (None, reason)."""
+    that summary was captured from THIS device code (its kernel id equals the
+    loaded library's), with the same launches per step and blocksizes.
+    Otherwise null, with the reason."""
     from paper_1904_05717_b200 import _native
 
-    bid = _native.build_id()
+    bid = _native.kernel_id()
     pdir = os.path.join(ROOT, "profiles")
     stale = None
     for name in sorted(os.listdir(pdir), reverse=True) if os.path.isdir(pdir) else []:
@@ -266,14 +267,15 @@ def ncu_traffic(workload, staging, launches_per_step):
             continue
         if d.get("workload") != workload or d.get("staging", "cpasync") != staging:
             continue
-        if d.get("build_id") != bid or d.get("launches_per_step") != launches_per_step or not d.get(
-                "dram_bytes_per_step"):
-            stale = stale or f"{name}: build {d.get('build_id')} / {d.get('launches_per_step')} launches per step"
+        if (d.get("kernel_id") != bid or d.get("launches_per_step") != launches_per_step
+                or not d.get("dram_bytes_per_step") or (blocksizes is not None and d.get("blocksizes") != blocksizes)):
+            stale = stale or (f"{name}: kernel {d.get('kernel_id')} / {d.get('launches_per_step')} launches per step"
+                              f" / blocksizes {d.get('blocksizes')}")
             continue
         return {"per_launch": d["dram_bytes_per_step"] / launches_per_step, "per_step": d["dram_bytes_per_step"],
-                "source": name, "build_id": bid}
-    return {"per_launch": None, "per_step": None, "source": None, "build_id": bid,
-            "why_null": (f"no ncu summary of build {bid} for this workload"
+                "source": name, "kernel_id": bid}
+    return {"per_launch": None, "per_step": None, "source": None, "kernel_id": bid,
+            "why_null": (f"no ncu summary of kernel build {bid} for this workload"
                          + (f" (stale: {stale})" if stale else ""))}
 
 
@@ -334,14 +336,13 @@ def reference_arm(args):
 
 # ------------------------------------------------------------------ our arm
 def make_plan(T, m, n, k, tile=128, family=FAMILY):
-    """The family member on the B200 hierarchy with the L2 level at its
-    effective capacity for residency (planner), blocksizes from the
+    """The family member on the device's derived B200 hierarchy
+    (planner.gpu_hierarchy_for: for the fused C-resident members, level 2 is
+    the co-resident wave's register-file C tiles), blocksizes from the
     reference's derivation with the GPU pins (planner.derive_for_gpu)."""
     from paper_1904_05717_b200 import planner as P
 
-    hier = P.gpu_hierarchy_effective(tile)
-    bs = P.derive_for_gpu(family, (m, n, k), hier, (tile, tile))
-    return T.build_plan(T.parse_name(family), bs, hier, T.Shape(m, n, k)), bs, hier
+    return P.plan_for_gpu(family, (m, n, k), "fused", (tile, tile))
 
 
 def verify_sampled(C, m, n, k, steps, seeds, c0_zero, samples=VERIFY_SAMPLES, a_round=None, ld=None,
@@ -433,8 +434,10 @@ def fp64_arm(args):
 
     peak = T.measure_fp64_peak(30)
     workload = workload_name(m, n, k, family)
-    traffic = ncu_traffic(workload, staging, launches_per_step)
+    bsd = {f"{lv}:{d}": v for (lv, d), v in bs.entries()}
+    traffic = ncu_traffic(workload, staging, launches_per_step, bsd)
     model = nest.model()
+    gmodel = nest.gpu_model(opts)
     hbm_model_bytes = model.at_level(hier.top_level()).total_bytes()
 
     # ---- e2e: host buffers through the C ABI, copies inside the timed region
@@ -477,11 +480,17 @@ def fp64_arm(args):
                      "kernel": kernel_name, "algorithmic_flops_per_launch": flops / launches_per_step,
                      "algorithmic_flops_per_step": flops, "launches_per_step": launches_per_step,
                      "traffic_per_step": traffic["per_step"], "traffic_source": traffic["source"],
-                     "build_id": traffic["build_id"], **({"traffic_null_because": traffic["why_null"]}
+                     "kernel_id": traffic["kernel_id"], **({"traffic_null_because": traffic["why_null"]}
                                                          if traffic["per_launch"] is None else {})},
         "model": {"hbm_bytes_model": hbm_model_bytes,
+                  "hbm_bytes_gpu_model": gmodel["hbm_total_bytes"],
+                  "smem_bytes_gpu_model": gmodel["smem_bytes"],
                   "hbm_bytes_measured": traffic["per_step"],
-                  "measured_over_model": (traffic["per_step"] / hbm_model_bytes) if traffic["per_step"] else None},
+                  "measured_over_model": (traffic["per_step"] / hbm_model_bytes) if traffic["per_step"] else None,
+                  "measured_over_gpu_model": (traffic["per_step"] / gmodel["hbm_total_bytes"])
+                  if traffic["per_step"] else None,
+                  "note": "hbm_bytes_model: the reference's multilevel_cost on the derived hierarchy; gpu_model: "
+                          "the schedule's own task list in lockstep through an LRU of the physical L2"},
         "verified": verified,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -593,7 +602,7 @@ def tc_arm(args):
                      "frac": achieved / peak, "traffic": traffic["per_launch"], "peak_source": src,
                      "tcgen05_issue_probe_tflops": probe, "kernel": "k_tc2<%s, 2> (256x512 SM pair, TMA epilogue)" % dtype,
                      "algorithmic_flops_per_launch": flops, "traffic_source": traffic["source"],
-                     "build_id": traffic["build_id"]},
+                     "kernel_id": traffic["kernel_id"]},
         "verified": verified, "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
         "gpu_launches": args.steps, "step_ms": step_ms,
     }

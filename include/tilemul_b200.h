@@ -114,9 +114,13 @@ const char* tm_last_error(void);
 /* Rule ids of the last failure, one per line "rule:level:lhs:rhs". */
 const char* tm_last_rules(void);
 const char* tm_version(void);
-/* sha256[:16] of the sources this library was built from (build.py
- * source_hash); ncu summaries under profiles/ carry the id they measured. */
+/* sha256[:16] of all the sources this library was built from (build.py
+ * source_hash); the Python loader refuses a library built from other sources. */
 const char* tm_build_id(void);
+/* sha256[:16] of the sources that decide the device work (kernels, lowering,
+ * host pipeline: build.py kernel_hash). ncu summaries under profiles/ carry
+ * the kernel id they measured; bench.py uses their bytes only on a match. */
+const char* tm_kernel_id(void);
 
 /* --- family descriptors (include/tilemul/descriptor.hpp) ---------------- */
 /* parse_name (:111-125): fills up to `cap` tiers, sets *count. */
@@ -167,6 +171,27 @@ int tm_plan_model(const tm_plan* plan, int64_t* out, int cap);
 /* multilevel_cost for any validated family member (no executable plan needed). */
 int tm_model(const char* name, int allow_non_c_registers, const tm_level* levels, int nlevels, int64_t m, int64_t n,
              int64_t k, const tm_blocksize* bs, int nbs, int64_t* out, int cap);
+/* GPU-mode I/O model of the schedule tm_execute would run with `opts` on a
+ * device with `sms` SMs and an L2 of `l2_bytes` (no GPU needed; gpu_model.cpp):
+ *   out[0..5]   elements into the SMEM level (L2 <-> SM), (reads, writes) for
+ *               A, B, C -- exact over the task list (FIFO staging: a task
+ *               streams m_t k_t of A and k_t n_t of B; C once in and out,
+ *               plus split-k partials);
+ *   out[6..11]  bytes across the HBM boundary, (read, written) for A, B, C,
+ *               from a lockstep run of the task list (one k-slab per CTA per
+ *               step, strided rounds or stream-K ranges as the kernel takes
+ *               them) through a write-back LRU of l2_bytes at slab granularity;
+ *   out[12..17] tasks, grid, lockstep steps, kernel id, tile_m, tile_n.
+ * elem_bytes: bytes per element of A, B, C (NULL = 8, 8, 8). Extends the
+ * reference's multilevel_cost (costmodel.hpp:163-229), which assumes a
+ * resident block per level and 8-byte elements. */
+int tm_plan_gpu_model(const tm_plan* plan, const tm_exec_opts* opts, int sms, int64_t l2_bytes,
+                      const double* elem_bytes, int64_t* out, int cap);
+/* The task list behind the model: 10 int32 per task (i0, j0, p0, m, n, k,
+ * slice, from_c, fixup, seq), the grid, and for stream-K the per-CTA task
+ * ranges (cta_first[0] = -1 when CTA c runs tasks c, c + grid, ...). */
+int tm_plan_tasks(const tm_plan* plan, const tm_exec_opts* opts, int sms, int32_t* tasks, int64_t cap,
+                  int64_t* count, int32_t* grid, int32_t* cta_first, int first_cap);
 /* Number of levels of the hierarchy the plan was validated against. */
 int tm_plan_levels(const tm_plan* plan);
 /* io_lower_bound (:67-76). */

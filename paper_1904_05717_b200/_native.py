@@ -57,6 +57,7 @@ SIGNATURES = [
     ("tm_last_rules", cstr, []),
     ("tm_version", cstr, []),
     ("tm_build_id", cstr, []),
+    ("tm_kernel_id", cstr, []),
     ("tm_parse_name", C.c_int, [cstr, C.c_int, C.POINTER(tm_tier), C.c_int, C.POINTER(C.c_int)]),
     ("tm_compose", C.c_int, [C.POINTER(i32), cstr, C.c_int, C.c_int, C.c_char_p, C.c_int, C.POINTER(tm_tier), C.c_int,
                              C.POINTER(C.c_int)]),
@@ -71,6 +72,9 @@ SIGNATURES = [
                                  C.POINTER(P)]),
     ("tm_plan_create_loops", C.c_int, [cstr, C.POINTER(tm_loop), C.c_int, i64, i64, i64, i64, i64, C.POINTER(P)]),
     ("tm_plan_destroy", None, [P]),
+    ("tm_plan_gpu_model", C.c_int, [P, C.POINTER(tm_exec_opts), C.c_int, i64, C.POINTER(dbl), C.POINTER(i64), C.c_int]),
+    ("tm_plan_tasks", C.c_int, [P, C.POINTER(tm_exec_opts), C.c_int, C.POINTER(i32), i64, C.POINTER(i64),
+                                C.POINTER(i32), C.POINTER(i32), C.c_int]),
     ("tm_ipc_export", C.c_int, [P, P, C.POINTER(i64)]),
     ("tm_ipc_open", C.c_int, [P, i64, C.POINTER(P)]),
     ("tm_ipc_close", C.c_int, [P, i64]),
@@ -141,6 +145,11 @@ def lib():
 def build_id() -> str:
     """The loaded library's build id (sha256[:16] of its sources)."""
     return lib().tm_build_id().decode()
+
+
+def kernel_id() -> str:
+    """The loaded library's kernel id (sha256[:16] of the device-work sources)."""
+    return lib().tm_kernel_id().decode()
 
 
 def declared_symbols():

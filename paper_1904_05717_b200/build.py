@@ -46,21 +46,40 @@ def source_files():
                   [os.path.join(ROOT, "include", "tilemul_b200.h"), os.path.abspath(__file__)])
 
 
-def source_hash() -> str:
-    """sha256[:16] over the library's sources (paths relative to the repo,
-    then contents): the build id compiled into the library (tm_build_id) and
-    stamped on every ncu summary, so a profile of another build is detected."""
+def kernel_files():
+    """The sources that decide the device work of an execute() call: the
+    kernels, the lowering onto CTA tasks, the host pipeline, the build flags."""
+    return sorted(glob.glob(os.path.join(CSRC, "kernels", "*")) +
+                  [os.path.join(CSRC, f) for f in ("lower.cpp", "engine.hpp", "host_pipe.cpp")] +
+                  [os.path.abspath(__file__)])
+
+
+def _hash(files) -> str:
     import hashlib
 
     h = hashlib.sha256()
-    for f in source_files():
+    for f in files:
         h.update(os.path.relpath(f, ROOT).replace(os.sep, "/").encode() + b"\0")
         h.update(open(f, "rb").read())
     return h.hexdigest()[:16]
 
 
+def source_hash() -> str:
+    """sha256[:16] over all of the library's sources (paths relative to the
+    repo, then contents): the build id compiled into the library
+    (tm_build_id); the loader refuses a library built from other sources."""
+    return _hash(source_files())
+
+
+def kernel_hash() -> str:
+    """sha256[:16] over kernel_files(): the kernel id (tm_kernel_id) stamped
+    on every ncu summary, so a profile of other device code is detected."""
+    return _hash(kernel_files())
+
+
 def _write_build_id() -> None:
-    text = f'#pragma once\n#define TM_BUILD_ID "{source_hash()}"\n'
+    text = (f'#pragma once\n#define TM_BUILD_ID "{source_hash()}"\n'
+            f'#define TM_KERNEL_ID "{kernel_hash()}"\n')
     if not os.path.exists(BUILD_ID) or open(BUILD_ID).read() != text:
         with open(BUILD_ID, "w") as f:
             f.write(text)

@@ -107,6 +107,18 @@ struct HostSchedule {
 };
 HostSchedule plan_tasks(const Nest& nest, const tm_exec_opts& o, gpu::Kernel kernel, int tile_m, int tile_n,
                         int slots);
+// GPU-mode I/O model of the schedule the kernel runs (gpu_model.cpp):
+// elements into the SMEM level per operand (exact over the task list) and
+// bytes crossing the HBM boundary from a lockstep run of the task list
+// through an LRU of the L2's capacity.
+struct GpuIo {
+    LevelFlow smem;
+    int64_t hbm_read_bytes[3] = {0, 0, 0}, hbm_write_bytes[3] = {0, 0, 0};
+    i64 tasks = 0, lockstep_slabs = 0;
+    int grid = 0, kernel = 0, tile_m = 0, tile_n = 0;
+};
+GpuIo gpu_io(const Nest& nest, const tm_exec_opts& o, int sms, int64_t l2_bytes, const double elem_bytes[3],
+             int policy = 0);
 // Tile shape and occupancy of a kernel: measured on the device (query) or
 // the compiled-in values (the model's CPU path).
 gpu::KernelInfo kernel_tiles(gpu::Kernel kernel, bool query);

@@ -1,15 +1,31 @@
 """GPU-aware planning: family members and blocksizes on
-the B200 hierarchy, ranked by the MOMMS I/O model.
+the B200 hierarchy, ranked by the GPU-mode I/O model.
 
 The reference's `select_algorithm` (descriptor.hpp:206-218) returns C for
 every BASELINE shape on a B200-sized L2 (its near/large tolerances never
 trigger), and its `derive_blocksizes` keeps each level's aspect
 ratio, which on the GPU hierarchy can squeeze a block below one CTA tile.
-This planner keeps the reference's derivation but (1) pins the dimensions the
-GPU realisation fixes — the SMEM-level m/n block = the CTA tile, and, when
-the aspect-preserving shrink makes a member infeasible, the L2 block's m/n
-side to a wave-sized extent — and (2) ranks every expressible member by the
-modelled traffic into L2 (the HBM boundary), then into SMEM.
+This planner keeps the reference's derivation but
+
+(1) sizes each level by where the member's resident block physically lives
+    on a B200 (gpu_hierarchy_for; no tuned constant):
+      level 0  the CTA's C tile (registers / TMEM), m_r x n_r;
+      level 1  shared memory per CTA (opt-in maximum);
+      level 2  for a C-resident top plan under the fused schedule: the
+               register files of the co-resident wave, G x m_r x n_r
+               (G = SMs x CTAs per SM) -- the fused schedule keeps every C
+               tile in registers for its whole k range, so the "L2 block" of
+               C is the set of tiles one wave holds while their A/B slabs
+               stream through L2; otherwise (A or B resident, or the faithful
+               schedule, whose cells round-trip C through L2): the physical
+               L2 (cudaDevAttrL2CacheSize);
+(2) pins the dimensions the GPU realisation fixes -- the SMEM-level m/n
+    block = the CTA tile, and, when the aspect-preserving shrink makes a
+    member infeasible, the L2 block's m/n side to a wave-sized extent;
+(3) ranks every expressible member by the GPU-mode model of the schedule the
+    kernel will run (LoopNest.gpu_model: FIFO-SMEM term exact over the task
+    list, HBM bytes from a lockstep run through an LRU of the physical L2),
+    then by the reference's own model.
 """
 from __future__ import annotations
 
@@ -22,24 +38,48 @@ from . import tilemul as T
 # (SURVEY.md §7.1): two cache levels, or one with the SMEM level skipped.
 GPU_MEMBERS = ("C2A1C0", "C2B1C0", "B2A1C0", "A2B1C0", "A2C0", "B2C0")
 WAVE_TILES = 12  # an L2 block side of 12 CTA tiles: 144 tiles ~ one wave on 148 SMs
-# Effective L2 capacity for MOMMS residency, as a fraction of the physical
-# 126 MiB. Measured (profiles/model_check_r01_l2frac_*.json): with the L2
-# level sized at 100% or 50%, C blocks derived by the reference's fit rules
-# do not stay resident (faithful C2A1C0 at 8192^3 moves 17x / 3.1x the
-# modelled HBM bytes); at 25% every faithful member lands within 0.95-1.03x
-# of the model and the fused schedule within 0.81-1.26x. The L2 is split
-# over two dies and also holds the streamed panels, so ~1/4 of it is what a
-# resident block can count on.
-L2_EFFECTIVE = 0.25
+# B200 facts used when no device is visible (planning on a CPU host): SMs,
+# shared memory per block (opt-in), L2 bytes -- the values the device reports.
+B200_SMS = 148
+B200_SMEM_OPTIN = 232448
+B200_L2_BYTES = T.B200_L2_BYTES
 
 
-def gpu_hierarchy_effective(tile: int = 128, l2_fraction: float = L2_EFFECTIVE) -> T.CacheHierarchy:
-    """The current device's {CTA tile, SMEM, L2} hierarchy with the L2 level
-    at its effective capacity for residency."""
-    h = T.gpu_hierarchy(tile)
-    caps = [h.capacity(i) for i in range(h.size())]
-    caps[-1] = max(caps[-2] + 1, int(caps[-1] * l2_fraction))
-    return T.CacheHierarchy.from_capacities(caps)
+def device_facts():
+    """(SMs, opt-in shared memory per block, L2 bytes) of the current CUDA
+    device, or the B200 values when none is visible."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            p = torch.cuda.get_device_properties(torch.cuda.current_device())
+            h = T.gpu_hierarchy(128)
+            return p.multi_processor_count, h.capacity(1) * 8, h.capacity(2) * 8
+    except Exception:  # noqa: BLE001 -- planning must work without a GPU
+        pass
+    return B200_SMS, B200_SMEM_OPTIN, B200_L2_BYTES
+
+
+def gpu_hierarchy_for(name: str, schedule: str = "fused", tile=(128, 128), facts=None,
+                      ctas_per_sm: int = 1) -> T.CacheHierarchy:
+    """The {C tile, SMEM, level 2} hierarchy in FP64 elements for family
+    member `name` under `schedule` (module doc, point 1)."""
+    sms, smem, l2 = facts or device_facts()
+    tile_el = tile[0] * tile[1]
+    top = T.parse_name(name).plans[0]
+    if schedule == "fused" and top.resident == "C" and top.level == 2:
+        lvl2 = sms * ctas_per_sm * tile_el  # the wave's register-file C tiles
+    else:
+        lvl2 = l2 // 8
+    return T.CacheHierarchy.from_capacities([tile_el, smem // 8, max(lvl2, smem // 8 + 1)])
+
+
+def plan_for_gpu(name: str, shape: Tuple[int, int, int], schedule: str = "fused", tile=(128, 128), facts=None):
+    """(nest, blocksizes, hierarchy) of member `name` on the device's derived
+    hierarchy -- the plan bench.py and the tests run."""
+    hier = gpu_hierarchy_for(name, schedule, tile, facts)
+    bs = derive_for_gpu(name, shape, hier, tile)
+    return T.build_plan(T.parse_name(name), bs, hier, T.Shape(*shape)), bs, hier
 
 
 @dataclass
@@ -49,6 +89,7 @@ class Candidate:
     hbm_bytes: float = float("inf")
     smem_bytes: float = float("inf")
     note: str = ""
+    hier: Optional[T.CacheHierarchy] = None
 
 
 def derive_for_gpu(name: str, shape: Tuple[int, int, int], hier: T.CacheHierarchy, tile=(128, 128),
@@ -85,18 +126,34 @@ def derive_for_gpu(name: str, shape: Tuple[int, int, int], hier: T.CacheHierarch
         return T.derive_blocksizes(d, hier, T.Shape(*shape), opts=opts, pinned=T.BlocksizeSet(pins))
 
 
-def rank_members(shape: Tuple[int, int, int], hier: T.CacheHierarchy, members=GPU_MEMBERS, tile=(128, 128),
-                 wave_block: bool = False, elem_bytes=None) -> List[Candidate]:
-    """Every member with its modelled bytes into L2 (top level) and SMEM
-    (level 1), cheapest first; infeasible members are kept with a note."""
+def rank_members(shape: Tuple[int, int, int], hier: Optional[T.CacheHierarchy] = None, members=GPU_MEMBERS,
+                 tile=(128, 128), wave_block: bool = False, elem_bytes=None, schedule: str = "fused",
+                 facts=None, gpu_mode: bool = True) -> List[Candidate]:
+    """Every member with its modelled bytes across the HBM boundary and into
+    SMEM, cheapest first; infeasible members are kept with a note.
+
+    gpu_mode (default): each member on its derived hierarchy
+    (gpu_hierarchy_for), costed by the GPU-mode model of the schedule the
+    kernel runs (LoopNest.gpu_model). gpu_mode=False: every member on the
+    given `hier`, costed by the reference's multilevel_cost."""
     eb = elem_bytes or {"A": 8, "B": 8, "C": 8}
     out = []
     for name in members:
         try:
-            bs = derive_for_gpu(name, shape, hier, tile, wave_block)
-            rep = T.multilevel_cost(T.parse_name(name), bs, hier, T.Shape(*shape))
-            out.append(Candidate(name, bs, rep.at_level(hier.top_level()).total_bytes(eb),
-                                 rep.at_level(1).total_bytes(eb)))
+            h = gpu_hierarchy_for(name, schedule, tile, facts) if (gpu_mode or hier is None) else hier
+            bs = derive_for_gpu(name, shape, h, tile, wave_block)
+            d = T.parse_name(name)
+            if gpu_mode:
+                nest = T.build_plan(d, bs, h, T.Shape(*shape))
+                sms = (facts or device_facts())[0]
+                g = nest.gpu_model(T.ExecOptions(schedule=schedule, split_k=0), sms=sms,
+                                   l2_bytes=(facts or device_facts())[2], elem_bytes=(eb["A"], eb["B"], eb["C"]))
+                out.append(Candidate(name, bs, float(g["hbm_total_bytes"]), float(g["smem_bytes"]),
+                                     hier=h))
+            else:
+                rep = T.multilevel_cost(d, bs, h, T.Shape(*shape))
+                out.append(Candidate(name, bs, rep.at_level(h.top_level()).total_bytes(eb),
+                                     rep.at_level(1).total_bytes(eb), hier=h))
         except (T.InfeasibleError, T.ValidationFailure, T.ParseError) as e:
             out.append(Candidate(name, None, note=f"{type(e).__name__}: {e}"))
     out.sort(key=lambda c: (c.hbm_bytes, c.smem_bytes, c.name))
@@ -104,17 +161,19 @@ def rank_members(shape: Tuple[int, int, int], hier: T.CacheHierarchy, members=GP
 
 
 def select_for_gpu(shape: Tuple[int, int, int], hier: Optional[T.CacheHierarchy] = None, tile=(128, 128),
-                   wave_block: bool = False):
-    """The cheapest member by the model, with the plan built: (nest, candidate).
-    Ties (equal modelled bytes) go to the member whose outermost resident the
-    reference's select_algorithm picks."""
-    hier = hier or gpu_hierarchy_effective(tile[0])
-    ranked = rank_members(shape, hier, tile=tile, wave_block=wave_block)
+                   wave_block: bool = False, facts=None):
+    """The cheapest member by the model, with the plan built: (nest, candidate,
+    ranking). With `hier` given, every member is derived on it and costed by
+    the reference's model; without, each on its derived GPU hierarchy and
+    costed by the GPU-mode model. Ties (equal modelled bytes) go to the
+    member whose outermost resident the reference's select_algorithm picks."""
+    ranked = rank_members(shape, hier, tile=tile, wave_block=wave_block, facts=facts, gpu_mode=hier is None)
     best = [c for c in ranked if c.blocksizes is not None]
     if not best:
         raise T.InfeasibleError(f"no GPU family member is feasible for shape {shape}")
-    ref_outer = T.select_algorithm(T.Shape(*shape), hier.capacity(hier.top_level()))
+    h0 = best[0].hier
+    ref_outer = T.select_algorithm(T.Shape(*shape), h0.capacity(h0.top_level()))
     top = [c for c in best if c.hbm_bytes == best[0].hbm_bytes]
     pick = next((c for c in top if c.name[0] == ref_outer), top[0])
-    nest = T.build_plan(T.parse_name(pick.name), pick.blocksizes, hier, T.Shape(*shape))
+    nest = T.build_plan(T.parse_name(pick.name), pick.blocksizes, pick.hier, T.Shape(*shape))
     return nest, pick, ranked

@@ -498,6 +498,7 @@ def pareto_sweep(outer_capacity: int, ratios: Sequence[float], shape: Shape,
 NUMERICS = {"dmma": 0, "fma": 1, "exact": 2}
 SCHEDULES = {"fused": 0, "faithful": 1}
 STAGINGS = {"auto": 0, "cpasync": 1, "tma": 2}
+B200_L2_BYTES = 132644864  # cudaDevAttrL2CacheSize on the B200s of this pool (126.5 MiB)
 STAGING_NAMES = {0: None, 1: "cpasync", 2: "tma"}
 
 
@@ -576,6 +577,42 @@ class LoopNest:  # plan.hpp:25-85
         raw = (C.c_int64 * (nh * 6))()
         _check(N.lib().tm_plan_model(self._ptr, raw, nh * 6))
         return _report(self.shape, raw, nh)
+
+    def gpu_model(self, opts: "ExecOptions" = None, sms: int = 148, l2_bytes: Optional[int] = None,
+                  elem_bytes: Sequence[float] = (8, 8, 8)) -> Dict[str, object]:
+        """GPU-mode I/O model of the schedule execute() runs with `opts`
+        (tm_plan_gpu_model; no GPU needed): elements into the SMEM level per
+        operand (exact over the task list, FIFO staging) and bytes across
+        the HBM boundary from a lockstep run of the task list through an LRU
+        of the L2 (default: the B200's 126.5 MiB, cudaDevAttrL2CacheSize)."""
+        o = (opts or ExecOptions())._c()
+        eb = (C.c_double * 3)(*elem_bytes)
+        out = (C.c_int64 * 18)()
+        _check(N.lib().tm_plan_gpu_model(self._ptr, C.byref(o), sms, l2_bytes or B200_L2_BYTES, eb, out, 18))
+        smem = {op: (out[2 * q], out[2 * q + 1]) for q, op in enumerate(OPERANDS)}
+        hbm = {op: (out[6 + 2 * q], out[6 + 2 * q + 1]) for q, op in enumerate(OPERANDS)}
+        smem_bytes = sum(elem_bytes[q] * (out[2 * q] + out[2 * q + 1]) for q in range(3))
+        return {"smem_elements": smem, "smem_bytes": smem_bytes, "hbm_bytes": hbm,
+                "hbm_total_bytes": sum(r + w for r, w in hbm.values()),
+                "hbm_read_bytes": sum(r for r, _ in hbm.values()),
+                "tasks": out[12], "grid": out[13], "lockstep_slabs": out[14], "kernel": out[15],
+                "tile": (out[16], out[17])}
+
+    def tasks(self, opts: "ExecOptions" = None, sms: int = 148):
+        """The lowered task list (host half of the lowering): list of dicts
+        (i0, j0, p0, m, n, k, slice, from_c, fixup, seq), the grid, and per-CTA
+        ranges for stream-K (None when CTA c runs tasks c, c + grid, ...)."""
+        o = (opts or ExecOptions())._c()
+        cnt, grid = C.c_int64(0), C.c_int32(0)
+        _check(N.lib().tm_plan_tasks(self._ptr, C.byref(o), sms, None, 0, C.byref(cnt), C.byref(grid), None, 0))
+        buf = (C.c_int32 * max(1, 10 * cnt.value))()
+        first = (C.c_int32 * (grid.value + 1))()
+        _check(N.lib().tm_plan_tasks(self._ptr, C.byref(o), sms, buf, cnt.value, C.byref(cnt), C.byref(grid), first,
+                                     grid.value + 1))
+        keys = ("i0", "j0", "p0", "m", "n", "k", "slice", "from_c", "fixup", "seq")
+        ts = [dict(zip(keys, buf[10 * q:10 * q + 10])) for q in range(cnt.value)]
+        ranges = None if first[0] == -1 else list(first)
+        return ts, grid.value, ranges
 
     def last_launch(self) -> Dict[str, int]:
         t, l, c = C.c_int64(0), C.c_int32(0), C.c_int32(0)

@@ -73,7 +73,7 @@ def checksum(A, B, C, C0, m, n, k):
 
 # --- the bench's own path: config 2 at 16384^3 (BENCH_r01 headline) --------
 def test_headline_16384_segmented_tma():
-    """bench.py's exact plan and options: C2A1C0 on the effective hierarchy,
+    """bench.py's exact plan and options: C2A1C0 on the derived hierarchy,
     fused DMMA, auto split (tail split of the last partial wave), auto
     staging = TMA in 14 segment launches of whole rounds. Sampled entries
     against the oracle, the checksum over all of C, and bitwise equality with
@@ -104,9 +104,7 @@ def test_headline_16384_segmented_tma():
 @pytest.mark.parametrize("name", P.GPU_MEMBERS)
 def test_8192_every_member_segmented(name):
     m = n = k = 8192
-    hier = P.gpu_hierarchy_effective(128)
-    bs = P.derive_for_gpu(name, (m, n, k), hier, (128, 128))
-    nest = T.build_plan(T.parse_name(name), bs, hier, T.Shape(m, n, k))
+    nest, bs, hier = P.plan_for_gpu(name, (m, n, k))
     A, B, C = filled(m, n, k, seeds=(21, 22, 23))
     C0 = C.clone()
     T.execute(nest, A, B, C, T.ExecOptions(split_k=0))

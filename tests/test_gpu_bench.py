@@ -42,7 +42,7 @@ def test_bench_line_ours():
     v = d["verified"]
     assert v["ok"] and v["samples"] == 64 and v["steps_accumulated"] == 6 and v["worst_err_over_bound"] <= 1.0
     # roofline.traffic is set only from an ncu summary of this very build (else null, with the reason)
-    assert d["roofline"]["build_id"]
+    assert d["roofline"]["kernel_id"]
     assert d["roofline"]["traffic"] is None or d["roofline"]["traffic_source"]
 
 

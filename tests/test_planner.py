@@ -9,7 +9,7 @@ from paper_1904_05717_b200 import planner as P
 from paper_1904_05717_b200 import tilemul as T
 
 B200 = T.CacheHierarchy.from_capacities([128 * 128, 232448 // 8, 132644864 // 8])
-B200_EFF = T.CacheHierarchy.from_capacities([128 * 128, 232448 // 8, int(132644864 // 8 * P.L2_EFFECTIVE)])
+FACTS = (148, 232448, 132644864)  # SMs, opt-in SMEM per block, L2 bytes of a B200
 
 
 @pytest.mark.parametrize("shape,best", [((65536, 256, 1024), {"B2A1C0"}),    # panel-panel: B resident at L2
@@ -18,7 +18,7 @@ B200_EFF = T.CacheHierarchy.from_capacities([128 * 128, 232448 // 8, int(1326448
                                         # the other streams; C moves once either way (4.50 vs 4.63 GB)
                                         ((16384, 16384, 256), {"A2B1C0", "B2A1C0"})])
 def test_selects_model_cheapest_member(shape, best):
-    nest, pick, ranked = P.select_for_gpu(shape, B200)
+    nest, pick, ranked = P.select_for_gpu(shape, B200)  # the reference's model on one hierarchy
     assert pick.name in best
     feasible = [c for c in ranked if c.blocksizes is not None]
     assert feasible[0].hbm_bytes == pick.hbm_bytes
@@ -40,8 +40,42 @@ def test_gpu_pins_make_register_tiles_whole():
     assert bs.get(2, "m") == P.WAVE_TILES * 128
 
 
-def test_effective_l2_shrinks_the_resident_block():
-    full = P.derive_for_gpu("C2A1C0", (16384, 16384, 16384), B200)
-    eff = P.derive_for_gpu("C2A1C0", (16384, 16384, 16384), B200_EFF)
-    assert eff.get(2, "m") < full.get(2, "m")
-    assert eff.get(2, "m") * eff.get(2, "n") <= B200_EFF.capacity(2)
+def test_derived_hierarchy_per_member_and_schedule():
+    """Level 2 holds the top plan's resident where it physically lives: the
+    wave's register-file C tiles (148 x 128 x 128) for a C-resident member
+    under the fused schedule, else the physical L2 -- no tuned fraction."""
+    h = P.gpu_hierarchy_for("C2A1C0", "fused", facts=FACTS)
+    assert [h.capacity(i) for i in range(3)] == [16384, 29056, 148 * 16384]
+    for name, sched in (("B2A1C0", "fused"), ("A2C0", "fused"), ("C2A1C0", "faithful")):
+        assert P.gpu_hierarchy_for(name, sched, facts=FACTS).capacity(2) == 132644864 // 8
+    nest, bs, hier = P.plan_for_gpu("C2A1C0", (16384, 16384, 16384), facts=FACTS)
+    # the derived C block is about one wave of tiles
+    tiles = (bs.get(2, "m") // 128) * (bs.get(2, "n") // 128)
+    assert 100 <= tiles <= 148, tiles
+
+
+@pytest.mark.parametrize("shape", [(8192, 8192, 8192), (16384, 16384, 16384)])
+def test_reference_model_on_derived_hierarchy_matches_gpu_mode_model(shape):
+    """With level 2 = the wave's register-file capacity, the reference's own
+    multilevel_cost of the fused C2A1C0 plan agrees with the GPU-mode model of
+    the schedule the kernel runs (lockstep task list through an LRU of the
+    physical L2) within 10 %: the derived capacity replaces round 1's fitted
+    25 % L2 fraction."""
+    nest, bs, hier = P.plan_for_gpu("C2A1C0", shape, facts=FACTS)
+    ref = nest.model().at_level(2).total_bytes()
+    g = nest.gpu_model(T.ExecOptions(split_k=0), sms=148, l2_bytes=132644864)
+    assert 0.9 < g["hbm_total_bytes"] / ref < 1.1, (g["hbm_total_bytes"], ref)
+
+
+@pytest.mark.parametrize("shape,best", [((65536, 256, 1024), {"A2C0", "B2A1C0", "B2C0", "C2A1C0", "C2B1C0"}),
+                                        ((512, 512, 131072), {"C2A1C0", "C2B1C0"}),
+                                        ((16384, 16384, 256), {"A2B1C0", "B2A1C0"})])
+def test_selects_gpu_mode_cheapest_member(shape, best):
+    """Without a hierarchy: each member on its derived hierarchy, costed by
+    the GPU-mode model of the fused schedule. (Panel-panel: every member but
+    A2B1C0 moves only the compulsory 8(mk + kn + 2mn) bytes.)"""
+    nest, pick, ranked = P.select_for_gpu(shape, facts=FACTS)
+    assert pick.name in best, [(c.name, c.hbm_bytes) for c in ranked]
+    feasible = [c for c in ranked if c.blocksizes is not None]
+    assert len(feasible) == len(P.GPU_MEMBERS)
+    assert all(feasible[i].hbm_bytes <= feasible[i + 1].hbm_bytes for i in range(len(feasible) - 1))

@@ -70,7 +70,8 @@ def main():
                     help="task-kernel launches in one step of the workload (TMA segments): the first N kernels "
                          "matching --kernel-regex in the capture are summed into *_per_step")
     ap.add_argument("--kernel-regex", default=r"k_dmma|k_tc|k_simt", help="which captured kernels are task kernels")
-    ap.add_argument("--build-id", default=None, help="library build id the capture ran (default: the local build)")
+    ap.add_argument("--kernel-id", default=None, help="library kernel id the capture ran (default: the local build)")
+    ap.add_argument("--blocksizes", default=None, help="JSON of the plan's blocksizes (bench config.blocksizes)")
     ap.add_argument("--out-dir", default=os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                                       "profiles"))
     a = ap.parse_args()
@@ -107,14 +108,14 @@ def main():
                          f"{a.launches_per_step}")
     step = task[:a.launches_per_step]
     top = step[0]
-    bid = a.build_id
+    bid = a.kernel_id
     if bid is None:
         import sys
 
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         from paper_1904_05717_b200 import _native
 
-        bid = _native.build_id()
+        bid = _native.kernel_id()
     per_step = {
         "launches_per_step": a.launches_per_step,
         "dram_bytes_per_step": sum(k.get("dram_bytes", 0.0) for k in step),
@@ -126,7 +127,8 @@ def main():
         "tag": a.tag,
         "staging": a.staging,
         "report": os.path.basename(a.rep),
-        "build_id": bid,
+        "kernel_id": bid,
+        "blocksizes": json.loads(a.blocksizes) if a.blocksizes else None,
         **per_step,
         "kernel": top["kernel"],
         "duration_s_under_ncu": top.get("duration"),

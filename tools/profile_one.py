@@ -28,8 +28,7 @@ def main():
     from paper_1904_05717_b200 import planner, tilemul as T
 
     m, n, k = (int(x) for x in a.shape.split(","))
-    hier = planner.gpu_hierarchy_effective(128)
-    bs = planner.derive_for_gpu(a.family, (m, n, k), hier)
+    _, bs, hier = planner.plan_for_gpu(a.family, (m, n, k))
     nest = T.build_plan(T.parse_name(a.family), bs, hier, T.Shape(m, n, k))
     P = a.ld_pad
     Ab = torch.empty(k * (m + P), dtype=torch.float64, device="cuda")
