@@ -38,9 +38,12 @@ KEYS = {
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
     "sm__cycles_elapsed.avg": "sm_cycles",
     "smsp__cycles_active.avg": "smsp_cycles_active",
+    "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
+    "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active": "dmma_pipe_pct_of_active",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active": "hmma_pipe_pct_of_active",
 }
 UNIT = {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1e-9, "usecond": 1e-6,
-        "msecond": 1e-3, "second": 1.0}
+        "msecond": 1e-3, "second": 1.0, "Ghz": 1e9, "Mhz": 1e6, "hz": 1.0}
 
 
 def raw(rep):
