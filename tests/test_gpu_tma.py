@@ -220,10 +220,13 @@ def test_tma_config1_golden_entries():
 
 
 def test_tma_long_launch_auto_stays_cpasync():
-    """A launch in which a CTA streams more than 8192 k-slabs: auto stays on
+    """A launch whose one task streams more than the 4096-slab TMA limit per
+    CTA and cannot be cut into segments (a single round): auto stays on
     cp.async (TMA CTAs drift apart over long launches and lose the wave's L2
-    sharing, profiles/tma_l2_r01.json); an explicit TMA launch is bitwise
-    equal. One 128 x 128 tile, k = 8193 slabs + 16."""
+    sharing, profiles/tma_l2_r01.json; longer task LISTS are segmented, see
+    test_gpu_baseline_shapes.py::test_headline_16384_segmented_tma); an
+    explicit TMA launch is bitwise equal. One 128 x 128 tile, k = 8193 slabs
+    + 16."""
     m = n = 128
     k = 32 * 8193 + 16
     nest = fused_nest(m, n, k)
