@@ -154,6 +154,8 @@ struct TcArgs {
     int32_t ntasks;
     int64_t m = 0, n = 0;   // C extents (the TMA epilogue's clipping bounds)
     int32_t tma_c = 0;      // 256 x 512 pair kernel: tmC maps C (16-byte aligned columns) for the TMA epilogue
+    int32_t clc = 0;        // pair kernels: tiles by cluster launch control (one cluster launched per tile,
+                            // running clusters cancel not-yet-started ones and take their tiles)
 };
 
 template <bool TF32>
@@ -453,6 +455,45 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
         : "memory");
 }
 
+// ---- cluster launch control (sm_100): dynamic persistent tiles ----
+// The grid launches one cluster per tile. A running cluster asks the hardware
+// to cancel a cluster that has not started yet (clusterlaunchcontrol.try_cancel)
+// and, if that succeeds, computes the canceled cluster's tile next. Tiles are
+// taken in launch order, by whichever cluster is free first -- the window of
+// tiles in flight stays a run of consecutive raster tiles, as with fresh
+// clusters -- while the running cluster keeps its TMEM, barriers and pipeline
+// (no launch, no refill, and the next tile's loads and MMAs overlap this
+// tile's epilogue). Query j (j = 1, 2, ...) has its 16-byte response
+// multicast into both CTAs' resp[(j-1) % 4] and completes their
+// clc_full[(j-1) % 4]; every role (both producers, the MMA issuer, every
+// epilogue warp) reads it and arrives on the leader's clc_empty[(j-1) % 4]
+// before the slot is reused four queries later.
+constexpr int kClcSlots = 4;
+__device__ __forceinline__ void clc_try_cancel(uint32_t resp, uint64_t* bar) {
+    asm volatile(
+        "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.multicast::cluster::all.b128 "
+        "[%0], [%1];\n" ::"r"(resp),
+        "r"(saddr(bar))
+        : "memory");
+}
+// -1: no cluster was left to cancel; else the canceled cluster's index
+__device__ __forceinline__ int clc_decode(uint32_t resp) {
+    uint32_t ok, x = 0;
+    asm volatile(
+        "{\n .reg .pred p;\n .reg .b128 r;\n ld.shared.b128 r, [%2];\n"
+        " clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n selp.u32 %0, 1, 0, p;\n"
+        " @p clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %1, r;\n}\n"
+        : "=r"(ok), "+r"(x)
+        : "r"(resp)
+        : "memory");
+    return ok ? static_cast<int>(x >> 1) : -1;
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_remote(uint32_t cluster_addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(cluster_addr),
+                 "r"(bytes)
+                 : "memory");
+}
+
 // NH = 256-column halves of the pair tile: 1 -> 256 x 256 per pair, two
 // TMEM accumulators (the next tile's MMAs overlap this tile's epilogue);
 // 2 -> 256 x 512 per pair, one accumulator filling TMEM (512 columns), 25 %
@@ -477,7 +518,7 @@ struct Tc2Geo {
     static constexpr int THREADS = 128 + 32 * EPI_WARPS;
     static constexpr uint32_t A_LAYOUT = TF32 ? 1u : 2u;
     static constexpr uint32_t A_SBO = TF32 ? 512u : 1024u;
-    static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+    static constexpr int SMEM = STAGES * STAGE + 1024 + 512;
 };
 
 template <bool TF32>
@@ -498,7 +539,14 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
     uint64_t* tfull = empty + G::STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* cl = tempty + 2;  // TMA epilogue: C quarter loads into the (then idle) stage ring, 3 buffers
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cl + 3);
+    uint64_t* clc_full = cl + 3;                // cluster launch control: response landed (both CTAs)
+    uint64_t* clc_empty = clc_full + kClcSlots;  // response read by every role (leader's copy counts)
+    uint4* clc_resp = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(clc_empty + kClcSlots) + 15) & ~uintptr_t(15));
+    // clc + TMA epilogue (256 x 512): the epilogue stages C through the stage ring, so the producer starts a
+    // cluster's next tile only once this CTA's epilogue is done with the ring (it warms L2 with the tile's
+    // first k-blocks meanwhile)
+    uint64_t* ring_free = reinterpret_cast<uint64_t*>(clc_resp + kClcSlots);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring_free + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -519,6 +567,11 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
             mbar_init(&tempty[s], 2 * G::EPI_WARPS);
         }
         for (int s = 0; s < 3; ++s) mbar_init(&cl[s], 1);
+        mbar_init(ring_free, 1);
+        for (int s = 0; s < kClcSlots; ++s) {
+            mbar_init(&clc_full[s], 1);
+            mbar_init(&clc_empty[s], 3 + 2 * G::EPI_WARPS);  // 2 producers, the MMA issuer, every epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 2) {
@@ -531,13 +584,54 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    // The cluster's tile sequence: its own tile, then (clc) the tiles of the clusters it cancels, or
+    // (static) every nclusters-th tile. Every role walks the same sequence.
+    // queries are numbered from 1 (the cluster's own tile needs none): query q uses slot (q-1) % kClcSlots,
+    // phase (q-1) / kClcSlots of its barriers
+    auto clc_issue = [&](int q) {  // leader's producer: query q, once query q - kClcSlots has been read by all
+        const int sl = (q - 1) % kClcSlots;
+        if (q > kClcSlots) mbar_wait(&clc_empty[sl], ((q - 1) / kClcSlots - 1) & 1);
+        mbar_expect_tx(&clc_full[sl], 16);
+        mbar_arrive_expect_tx_remote(mapa_rank(&clc_full[sl], 1), 16);
+        clc_try_cancel(saddr(&clc_resp[sl]), &clc_full[sl]);
+    };
+    auto next_tile = [&](int ti, int& j, bool arrive) {  // arrive: this thread is its role's counted one
+        if (!a.clc) return ti + nclusters;
+        ++j;
+        const int sl = (j - 1) % kClcSlots;
+        mbar_wait(&clc_full[sl], ((j - 1) / kClcSlots) & 1);
+        const int t = clc_decode(saddr(&clc_resp[sl]));
+        if (arrive) mbar_arrive_remote(mapa_rank(&clc_empty[sl], 0));
+        return t < 0 ? a.ntasks : t;
+    };
+
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer (both CTAs)
             int stage = 0;
             uint32_t phase = 0;
-            for (int ti = cluster; ti < a.ntasks; ti += nclusters) {
+            int j = 0;
+            uint32_t ntile = 0;
+            const bool gate = NH == 2 && a.clc && a.tma_c;
+            if (a.clc && leader) clc_issue(1);
+            for (int ti = cluster; ti < a.ntasks; ++ntile) {
                 const Task t = a.tasks[ti];
                 const int nk = (t.k + G::BK - 1) / G::BK;
+                if (gate && ntile > 0) {
+                    for (int kb = 0; kb < nk && kb < G::STAGES; ++kb) {
+                        const int kc = t.p0 + kb * G::BK;
+                        for (int h = 0; h < G::A_BOXES; ++h)
+                            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                                             reinterpret_cast<uint64_t>(&tmA)),
+                                         "r"(t.i0 + static_cast<int>(rank) * 128 + h * G::MATOM), "r"(kc)
+                                         : "memory");
+                        for (int h = 0; h < NH; ++h)
+                            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                                             reinterpret_cast<uint64_t>(&tmB)),
+                                         "r"(kc), "r"(t.j0 + h * 256 + static_cast<int>(rank) * 128)
+                                         : "memory");
+                    }
+                    mbar_wait(ring_free, (ntile - 1) & 1);
+                }
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (NH == 2 && a.tma_c && kb == nk - TC_CPF_AHEAD) {
@@ -566,6 +660,8 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
                         phase ^= 1;
                     }
                 }
+                ti = next_tile(ti, j, true);
+                if (a.clc && leader && ti < a.ntasks) clc_issue(j + 1);  // one tile ahead
             }
         }
     } else if (warp == 1) {
@@ -575,7 +671,8 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
             uint32_t phase = 0;
             int acc = 0;
             uint32_t aphase = 0;
-            for (int ti = cluster; ti < a.ntasks; ti += nclusters) {
+            int j = 0;
+            for (int ti = cluster; ti < a.ntasks; ti = next_tile(ti, j, true)) {
                 const Task t = a.tasks[ti];
                 const int nk = (t.k + G::BK - 1) / G::BK;
                 mbar_wait(&tempty[acc], aphase ^ 1);
@@ -614,7 +711,8 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
         int acc = 0;
         uint32_t aphase = 0;
         uint32_t ntask = 0;
-        for (int ti = cluster; ti < a.ntasks; ti += nclusters, ++ntask) {
+        int j = 0;
+        for (int ti = cluster; ti < a.ntasks; ti = next_tile(ti, j, lane == 0), ++ntask) {
             const Task t = a.tasks[ti];
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
@@ -625,7 +723,7 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
             if constexpr (NH == 2) {
                 const bool covers = (t.m == 256 || static_cast<int64_t>(t.i0) + t.m == a.m) &&
                                     (t.n == 512 || static_cast<int64_t>(t.j0) + t.n == a.n);
-                if (a.tma_c && covers && a.ntasks <= nclusters) {
+                if (a.tma_c && covers && (a.ntasks <= nclusters || a.clc)) {
                     constexpr uint32_t QB = 128 * 128 * 4;  // bytes of one quarter
                     const uint32_t cbase = saddr(smem);
                     const int r0 = t.i0 + static_cast<int>(rank) * 128;
@@ -664,7 +762,10 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
                             }
                         }
                     }
-                    if (issuer) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+                    if (issuer) {
+                        asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+                        if (a.clc) mbar_arrive(ring_free);  // the ring is the producer's again
+                    }
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_remote(mapa_rank(&tempty[acc], 0));
@@ -675,6 +776,7 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
                     continue;
                 }
             }
+            if (NH == 2 && a.clc && a.tma_c && warp == 4 && lane == 0) mbar_arrive(ring_free);  // (ring untouched)
             const bool live = row < t.m;
             float* crow = a.C + (static_cast<int64_t>(t.i0) + row) + static_cast<int64_t>(t.j0 + h * 256) * a.ldc;
 #pragma unroll 1
@@ -827,6 +929,16 @@ cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb,
         }();
         args.tma_c &= tma_epilogue_knob;
     }
+    // Cluster launch control: on for the persistent 256 x 256 kernel (its static stride let the clusters
+    // drift apart: 16384^3 bf16 18.6 -> 12.0 GB of HBM reads, 1250 -> 1300 TF/s; tf32 681 -> 712), off for
+    // the 256 x 512 kernel, which already runs one fresh cluster per tile (CLC measured neutral there:
+    // 1353 vs 1345-1372 TF/s, the TMA epilogue then gated on the stage ring; profiles/ab_r02_tc_clc.json).
+    static const int clc_knob = [] {  // TILEMUL_TC_CLC=0/1: A/B knob for both kernels
+        const char* env = std::getenv("TILEMUL_TC_CLC");
+        return env ? std::atoi(env) : -1;
+    }();
+    args.clc = clc_knob < 0 ? (NH == 1 ? 1 : 0) : clc_knob;
+    if (args.clc) grid = 2 * ntasks;  // one cluster per tile; running clusters take the unstarted ones' tiles
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
     cfg.blockDim = dim3(G::THREADS);
