@@ -65,6 +65,13 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
                  "r"(src), "r"(c0), "r"(c1)
                  : "memory");
 }
+// C += box, the add done by the L2 (TMA reduction): the epilogue never reads C into the SM
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(c0), "r"(c1)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load_2d_cta(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(dst),
@@ -154,6 +161,7 @@ struct TcArgs {
     int32_t ntasks;
     int64_t m = 0, n = 0;   // C extents (the TMA epilogue's clipping bounds)
     int32_t tma_c = 0;      // 256 x 512 pair kernel: tmC maps C (16-byte aligned columns) for the TMA epilogue
+    int32_t tma_red = 0;    // 256 x 512 TMA epilogue: C += acc by TMA reduce-add in L2 (no C load)
     int32_t clc = 0;        // pair kernels: tiles by cluster launch control (one cluster launched per tile,
                             // running clusters cancel not-yet-started ones and take their tiles)
 };
@@ -729,6 +737,49 @@ __global__ void __launch_bounds__(Tc2Geo<TF32, NH>::THREADS, 1) k_tc2(const __gr
                     const int r0 = t.i0 + static_cast<int>(rank) * 128;
                     const bool issuer = warp == 4 && lane == 0;
                     const uint32_t ph = ntask & 1;  // cl[1], cl[2] complete once per task, cl[0] twice
+                    if (a.tma_red) {
+                        // Reduction epilogue: each lane writes its TMEM row of a quarter into a ring buffer and
+                        // one thread issues a TMA reduce-add of the quarter onto C -- the L2 adds, so C is
+                        // never loaded into the SM (one SMEM pass per quarter instead of load + read + write +
+                        // store). Quarter 3 reuses buffer 0 once quarter 0's reduction has read it.
+                        const int g = (warp - 4) >> 2;
+                        for (int q = 0; q < 4; ++q) {
+                            const int buf = q % 3;
+                            if (q == 3) {
+                                if (issuer) asm volatile("cp.async.bulk.wait_group.read 2;\n" ::: "memory");
+                                asm volatile("bar.sync 1, %0;\n" ::"n"(32 * G::EPI_WARPS) : "memory");
+                            }
+                            float* cs = reinterpret_cast<float*>(smem + buf * QB);
+#pragma unroll 1
+                            for (int cc = 0; cc < 2; ++cc) {
+                                const int col = g * 64 + cc * 32;
+                                uint32_t r[32];
+                                TC_LD32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) +
+                                            static_cast<uint32_t>(q * 128 + col), r);
+                                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) cs[(col + j) * 128 + ew * 32 + lane] = __uint_as_float(r[j]);
+                            }
+                            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                            asm volatile("bar.sync 1, %0;\n" ::"n"(32 * G::EPI_WARPS) : "memory");
+                            if (issuer) {
+                                tma_reduce_add_2d(&tmC, cbase + buf * QB, r0, t.j0 + q * 128);
+                                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                            }
+                        }
+                        if (issuer) {
+                            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                            if (a.clc) mbar_arrive(ring_free);  // the ring is the producer's again
+                        }
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(mapa_rank(&tempty[acc], 0));
+                        if (++acc == G::NACC) {
+                            acc = 0;
+                            aphase ^= 1;
+                        }
+                        continue;
+                    }
                     if (issuer) {
                         for (int q = 0; q < 3; ++q) {
                             mbar_expect_tx(&cl[q], QB);
@@ -928,6 +979,11 @@ cudaError_t launch_tc2_t(const void* A, int64_t lda, const void* B, int64_t ldb,
             return env ? std::atoi(env) : 1;
         }();
         args.tma_c &= tma_epilogue_knob;
+        static const int tma_red_knob = [] {  // TILEMUL_TC_TMA_REDUCE: A/B knob
+            const char* env = std::getenv("TILEMUL_TC_TMA_REDUCE");
+            return env ? std::atoi(env) : 1;
+        }();
+        args.tma_red = args.tma_c && tma_red_knob;
     }
     // Cluster launch control: on for the persistent 256 x 256 kernel (its static stride let the clusters
     // drift apart: 16384^3 bf16 18.6 -> 12.0 GB of HBM reads, 1250 -> 1300 TF/s; tf32 681 -> 712), off for
