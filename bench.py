@@ -626,6 +626,9 @@ def our_arm(args):
     if world > 1 or args.summa or args.config == "5":
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29541")
+        if world > 1:  # communicator init lines (rank, device, NVLink/NVLS transport) for the run's record
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
         from paper_1904_05717_b200 import multigpu
 
