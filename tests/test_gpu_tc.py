@@ -137,3 +137,33 @@ def test_tc_peak_probe():
     assert 0.4 < tf32 / bf16 < 0.6
     with pytest.raises(ValueError):
         T.measure_tc_peak("fp8", 1)
+
+
+# The A/B knobs of the pair kernels are read once per process, so their non-default settings run in
+# child processes: cluster launch control on the 256 x 512 kernel (TMA epilogue gated on the stage
+# ring), off on the 256 x 256 kernel (static persistent stride), and the load-add-store epilogue in place
+# of the TMA reduce-add. Shapes with several waves of tiles, so running clusters take unstarted tiles.
+KNOB_CASES = [
+    ({"TILEMUL_TC_CLC": "1"}, 256, 0),
+    ({"TILEMUL_TC_CLC": "0"}, 256, 256),
+    ({"TILEMUL_TC_TMA_REDUCE": "0"}, 256, 0),
+    ({"TILEMUL_TC_TMA_EPILOGUE": "0"}, 256, 0),
+]
+
+
+@pytest.mark.parametrize("env,tile,tile_n", KNOB_CASES)
+def test_tc_knob_variants_in_child_process(env, tile, tile_n):
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "import test_gpu_tc as M\n"
+            "for dt in ('bf16', 'tf32'):\n"
+            "    M.run_case(4096, 4608, 320, dt, sample=4096, tile=%d, tile_n=%d)\n"
+            "    M.run_case(1000, 1304, 200, dt, tile=%d, tile_n=%d)\n"
+            "print('ok')\n") % (root, os.path.join(root, "tests"), tile, tile_n, tile, tile_n)
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-2000:]
