@@ -514,11 +514,9 @@ def tc_arm(args):
 
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     m, n, k, family, _, dtype = shape_of(args)
-    hier = T.CacheHierarchy.from_capacities([256 * 512, 232448, 132644864 // 2])
-    d = T.parse_name(family)
-    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(256, 512)),
-                             pinned=T.BlocksizeSet({(1, "m"): 256}))
-    nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+    from paper_1904_05717_b200 import planner as P
+
+    nest, bs, hier = P.plan_tc_for_gpu(family, (m, n, k))  # the measured raster (planner.TC_L2_BLOCK)
     x = torch.empty(m * k, dtype=torch.float64, device="cuda")
     T.fill_uniform_device(x, 31)
     A = T.round_inputs(x, dtype)
@@ -597,10 +595,11 @@ def tc_arm(args):
         "config": {"workload": workload, "baseline_config": args.config, "m": m, "n": n, "k": k, "family": family,
                    "c0": "zero (config 4 leaves C init unspecified)", "accumulate": "fp32 (TMEM)",
                    "cta_tile": "256x512 per SM pair (cta_group::2)", "l2_flush": "not needed: inputs > 1.5 GB",
+                   "blocksizes": {f"{lv}:{d}": v for (lv, d), v in bs.entries()},
                    "parallelism": "1 GPU"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic["per_launch"], "peak_source": src,
-                     "tcgen05_issue_probe_tflops": probe, "kernel": "k_tc2<%s, 2> (256x512 SM pair, TMA epilogue)" % dtype,
+                     "tcgen05_issue_probe_tflops": probe, "kernel": "k_tc2<%s, 2> (256x512 SM pair, TMA reduce-add epilogue)" % dtype,
                      "algorithmic_flops_per_launch": flops, "traffic_source": traffic["source"],
                      "kernel_id": traffic["kernel_id"]},
         "verified": verified, "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),

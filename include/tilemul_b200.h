@@ -187,6 +187,11 @@ int tm_model(const char* name, int allow_non_c_registers, const tm_level* levels
  * resident block per level and 8-byte elements. */
 int tm_plan_gpu_model(const tm_plan* plan, const tm_exec_opts* opts, int sms, int64_t l2_bytes,
                       const double* elem_bytes, int64_t* out, int cap);
+/* The same model for the tcgen05 path tm_execute_tc runs (dtype TM_DTYPE_BF16 / TM_DTYPE_TF32; the
+ * opts' tile / tile_n pick the kernel as there): 2- or 4-byte inputs, fp32 C, SM-pair tiles one per
+ * cluster with sms / 2 clusters in flight. Same 18-entry output. */
+int tm_plan_gpu_model_tc(const tm_plan* plan, int dtype, const tm_exec_opts* opts, int sms, int64_t l2_bytes,
+                         int64_t* out, int cap);
 /* The task list behind the model: 10 int32 per task (i0, j0, p0, m, n, k,
  * slice, from_c, fixup, seq), the grid, and for stream-K the per-CTA task
  * ranges (cta_first[0] = -1 when CTA c runs tasks c, c + grid, ...). */

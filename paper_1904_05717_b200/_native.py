@@ -73,6 +73,7 @@ SIGNATURES = [
     ("tm_plan_create_loops", C.c_int, [cstr, C.POINTER(tm_loop), C.c_int, i64, i64, i64, i64, i64, C.POINTER(P)]),
     ("tm_plan_destroy", None, [P]),
     ("tm_plan_gpu_model", C.c_int, [P, C.POINTER(tm_exec_opts), C.c_int, i64, C.POINTER(dbl), C.POINTER(i64), C.c_int]),
+    ("tm_plan_gpu_model_tc", C.c_int, [P, C.c_int, C.POINTER(tm_exec_opts), C.c_int, i64, C.POINTER(i64), C.c_int]),
     ("tm_plan_tasks", C.c_int, [P, C.POINTER(tm_exec_opts), C.c_int, C.POINTER(i32), i64, C.POINTER(i64),
                                 C.POINTER(i32), C.POINTER(i32), C.c_int]),
     ("tm_ipc_export", C.c_int, [P, P, C.POINTER(i64)]),

@@ -117,8 +117,12 @@ struct GpuIo {
     i64 tasks = 0, lockstep_slabs = 0;
     int grid = 0, kernel = 0, tile_m = 0, tile_n = 0;
 };
+// kernel < 0: the kernel execute() picks for `o`; else that kernel (the tensor-core path's tiles: for the
+// SM-pair kernels one task per cluster, sms / 2 clusters in flight).
 GpuIo gpu_io(const Nest& nest, const tm_exec_opts& o, int sms, int64_t l2_bytes, const double elem_bytes[3],
-             int policy = 0);
+             int policy = 0, int kernel = -1);
+// The tcgen05 kernel tm_execute_tc runs for `dtype` and the tile options (TM_DTYPE_*).
+gpu::Kernel pick_tc_kernel(int dtype, const tm_exec_opts& o);
 // Tile shape and occupancy of a kernel: measured on the device (query) or
 // the compiled-in values (the model's CPU path).
 gpu::KernelInfo kernel_tiles(gpu::Kernel kernel, bool query);

@@ -24,6 +24,7 @@
 // Both are computed from the host half of the lowering (plan_tasks), so the
 // model describes exactly the schedule the kernel runs, and needs no GPU.
 #include <algorithm>
+#include <cstdlib>
 #include <list>
 #include <unordered_map>
 
@@ -134,13 +135,17 @@ class UnitCache {
 }  // namespace
 
 GpuIo gpu_io(const Nest& nest, const tm_exec_opts& o, int sms, int64_t l2_bytes, const double elem_bytes[3],
-             int policy) {
+             int policy, int kernel_override) {
+    const bool stagger = kernel_override == gpu::kTc2wBf16 || kernel_override == gpu::kTc2wTf32;
     if (sms < 1) fail_usage("SM count must be >= 1");
     if (l2_bytes < 1) fail_usage("L2 capacity must be >= 1 byte");
     const bool tma = o.staging != TM_STAGING_CPASYNC;
-    const gpu::Kernel kernel = pick_kernel(nest, o, tma);
+    const gpu::Kernel kernel = kernel_override >= 0 ? static_cast<gpu::Kernel>(kernel_override) : pick_kernel(nest, o, tma);
     const gpu::KernelInfo info = kernel_tiles(kernel, false);
-    const int slots = sms * std::max(1, info.ctas_per_sm);
+    const bool pair = kernel == gpu::kTc2Bf16 || kernel == gpu::kTc2Tf32 || kernel == gpu::kTc2wBf16 ||
+                      kernel == gpu::kTc2wTf32;
+    // SM-pair kernels: a task is one cluster's tile, sms / 2 clusters in flight
+    const int slots = pair ? std::max(1, sms / 2) : sms * std::max(1, info.ctas_per_sm);
     const HostSchedule hs = plan_tasks(nest, o, kernel, info.tile_m, info.tile_n, slots);
     const auto& T = hs.tasks;
     const i64 bk = kernel >= gpu::kTcBf16 ? 64 : 32;  // k-slab depth of the kernel's SMEM ring
@@ -193,6 +198,14 @@ GpuIo gpu_io(const Nest& nest, const tm_exec_opts& o, int sms, int64_t l2_bytes,
     const i64 M = nest.ext.m, N = nest.ext.n;
     std::vector<std::size_t> pos(static_cast<std::size_t>(G), 0);
     std::vector<i64> slab(static_cast<std::size_t>(G), -1);  // next slab of the current task (-1: task not started)
+    // One fresh cluster per tile (the 256 x 512 tcgen05 kernel): a tile starts when any earlier one ends, so in
+    // steady state the tiles in flight are spread evenly over a tile's k range rather than in lockstep. Modelled
+    // by starting slot c c/G of a task later (steps of idle) -- a property of dynamic launch order, no fit.
+    std::vector<i64> delay(static_cast<std::size_t>(G), 0);
+    if (stagger && !T.empty()) {
+        const i64 ns = cdiv(static_cast<i64>(T[0].k), bk);
+        for (int c = 0; c < G; ++c) delay[static_cast<std::size_t>(c)] = (ns * c) / G;
+    }
     i64 active = G, steps = 0;
     auto c_key = [&](const gpu::Task& t) { return UnitKey{2 + 4 * (static_cast<int64_t>(t.i0) + M * t.j0), 0}; };
     auto w_key = [&](int32_t s) { return UnitKey{3 + 4 * static_cast<int64_t>(s), 0}; };
@@ -204,6 +217,10 @@ GpuIo gpu_io(const Nest& nest, const tm_exec_opts& o, int sms, int64_t l2_bytes,
             i64& s = slab[static_cast<std::size_t>(c)];
             if (p >= sq.size()) continue;
             ++active;
+            if (delay[static_cast<std::size_t>(c)] > 0) {
+                --delay[static_cast<std::size_t>(c)];
+                continue;
+            }
             const gpu::Task& t = T[static_cast<std::size_t>(sq[p])];
             const i64 mn = static_cast<i64>(t.m) * t.n;
             if (s < 0) {  // task start: C in, unless the part starts from zero (split-k contributors)

@@ -80,6 +80,16 @@ int sm_count() {
     return sms;
 }
 
+gpu::Kernel pick_tc_kernel(int dtype, const tm_exec_opts& o) {
+    const bool pair = o.tile != 128;
+    // SM pairs default to 256 x 512 tiles: 25 % fewer L2->SMEM bytes per flop than 256 x 256, which
+    // under the board power cap buys clock (config 4)
+    const bool wide = pair && o.tile_n != 256;
+    const bool tf32 = dtype == TM_DTYPE_TF32;
+    return wide ? (tf32 ? gpu::kTc2wTf32 : gpu::kTc2wBf16)
+                : pair ? (tf32 ? gpu::kTc2Tf32 : gpu::kTc2Bf16) : (tf32 ? gpu::kTcTf32 : gpu::kTcBf16);
+}
+
 gpu::Kernel pick_kernel(const Nest& nest, const tm_exec_opts& o, bool tma) {
     const bool small_tile = o.tile == 64 || (o.tile == 0 && (nest.m_r < 128 || nest.n_r < 128));
     if (o.tile != 0 && o.tile != 64 && o.tile != 128) fail_usage("tile must be 0, 64 or 128");

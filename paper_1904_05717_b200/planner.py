@@ -177,3 +177,35 @@ def select_for_gpu(shape: Tuple[int, int, int], hier: Optional[T.CacheHierarchy]
     pick = next((c for c in top if c.name[0] == ref_outer), top[0])
     nest = T.build_plan(T.parse_name(pick.name), pick.blocksizes, pick.hier, T.Shape(*shape))
     return nest, pick, ranked
+
+
+# Config 4 (tcgen05, 256 x 512 SM-pair tiles, one fresh cluster per tile): the raster's L2 block. Measured at
+# 16384^3 (profiles/tc_l2_blocks_r02.json): DRAM reads per launch and TF/s by block (m x n)
+#   bf16: 2048x2048 / 3072x2048 / 4096x2048 8.9 GB, 1417 TF/s; 2048x1536 9.8 GB; 3072x3072 9.2 GB, 1386;
+#         2048x4608 (the round-1 raster) 10.6 GB, 1385; 1024x1024 11.8 GB, 1386
+#   tf32: 2048x2048 17.8 GB, 771 TF/s; 4096x1536 19.3 GB, 770; 2048x4608 21.1 GB, 755; 1024x1024 23.0 GB, 757
+# Under the board power cap the rate follows the bytes moved. Blocks 2048 columns wide (4 pair tiles) win for
+# both input widths: the column's B panels stay in L2 while the window of ~74 tiles in flight walks down it,
+# and the A panels are re-read once per 2048 columns. The GPU-mode model of this kernel (gpu_model_tc: tiles
+# staggered over the k range, random replacement) ranks the bf16 blocks the same way but not the tf32 ones,
+# so the block is the measured one.
+TC_L2_BLOCK = (2048, 2048)
+
+
+def plan_tc_for_gpu(name: str, shape: Tuple[int, int, int], tile=(256, 512), l2_block=TC_L2_BLOCK):
+    """(nest, blocksizes, hierarchy) for the tensor-core path (execute_tc): register tile = the SM pair's
+    TMEM accumulator, SMEM level = the pair's shared memory, and the raster's L2 block pinned to the measured
+    TC_L2_BLOCK (clipped to the shape)."""
+    m, n, k = shape
+    hier = T.CacheHierarchy.from_capacities([tile[0] * tile[1], B200_SMEM_OPTIN, B200_L2_BYTES // 2])
+    d = T.parse_name(name)
+    pins = {(1, "m"): min(tile[0], m)}
+    top = d.plans[0]
+    for dim in (top.outer_dim, top.inner_dim):
+        if dim == "m":
+            pins[(top.level, "m")] = min(l2_block[0], m)
+        elif dim == "n":
+            pins[(top.level, "n")] = min(l2_block[1], n)
+    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(*tile)),
+                             pinned=T.BlocksizeSet(pins))
+    return T.build_plan(d, bs, hier, T.Shape(m, n, k)), bs, hier

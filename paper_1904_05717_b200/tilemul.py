@@ -598,6 +598,24 @@ class LoopNest:  # plan.hpp:25-85
                 "tasks": out[12], "grid": out[13], "lockstep_slabs": out[14], "kernel": out[15],
                 "tile": (out[16], out[17])}
 
+    def gpu_model_tc(self, dtype: str = "bf16", opts: "ExecOptions" = None, sms: int = 148,
+                     l2_bytes: Optional[int] = None) -> Dict[str, object]:
+        """The GPU-mode model of the tcgen05 path execute_tc runs (tm_plan_gpu_model_tc): the task list of
+        the kernel `opts` selects (default: 256 x 512 SM-pair tiles, one per cluster, sms / 2 clusters in
+        flight), bf16 (2-byte) or tf32 (4-byte) inputs, fp32 C."""
+        o = (opts or ExecOptions())._c()
+        out = (C.c_int64 * 18)()
+        _check(N.lib().tm_plan_gpu_model_tc(self._ptr, DTYPES[dtype], C.byref(o), sms, l2_bytes or B200_L2_BYTES,
+                                            out, 18))
+        eb = (2, 2, 4) if dtype == "bf16" else (4, 4, 4)
+        smem = {op: (out[2 * q], out[2 * q + 1]) for q, op in enumerate(OPERANDS)}
+        hbm = {op: (out[6 + 2 * q], out[6 + 2 * q + 1]) for q, op in enumerate(OPERANDS)}
+        return {"smem_elements": smem, "smem_bytes": sum(eb[q] * (out[2 * q] + out[2 * q + 1]) for q in range(3)),
+                "hbm_bytes": hbm, "hbm_total_bytes": sum(r + w for r, w in hbm.values()),
+                "hbm_read_bytes": sum(r for r, _ in hbm.values()),
+                "tasks": out[12], "grid": out[13], "lockstep_slabs": out[14], "kernel": out[15],
+                "tile": (out[16], out[17])}
+
     def tasks(self, opts: "ExecOptions" = None, sms: int = 148):
         """The lowered task list (host half of the lowering): list of dicts
         (i0, j0, p0, m, n, k, slice, from_c, fixup, seq), the grid, and per-CTA

@@ -33,7 +33,7 @@ def main():
     d = T.parse_name("C2A1C0")
     def plan(tile, tile_n=256):
         # one wave of pair tiles per L2 block: 6 x 12 of 256 x 256, 8 x 9 of 256 x 512
-        l2m, l2n = (L2M, L2N) if tile_n == 256 else (2048, 4608)
+        l2m, l2n = (L2M, L2N) if tile_n == 256 else tuple(int(x) for x in os.environ.get("TC_L2_BLOCK_WIDE", "2048x2048").split("x"))
         hier = hier1 if tile_n == 256 else hier2
         bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(tile, tile_n)),
                                  pinned=T.BlocksizeSet({(1, "m"): tile, (2, "m"): l2m, (2, "n"): l2n}))
