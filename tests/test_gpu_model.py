@@ -216,3 +216,28 @@ def test_wave_model_explains_the_raster():
     waves = (m // 128) * (n // 128) // 16
     assert gs["hbm_bytes"]["A"][0] + gs["hbm_bytes"]["B"][0] == waves * 8 * 8 * 128 * k
     assert gr["hbm_bytes"]["A"][0] + gr["hbm_bytes"]["B"][0] == waves * 17 * 8 * 128 * k
+
+
+@pytest.mark.parametrize("dtype,eb", [("bf16", 2), ("tf32", 4)])
+def test_tc_model_fifo_term_and_bounds(dtype, eb):
+    """The tcgen05 path's model (gpu_model_tc): 256 x 512 SM-pair tiles, one per cluster, sms/2 clusters
+    in flight, 2- or 4-byte inputs and fp32 C. Its SMEM term is the FIFO closed form over those tiles
+    (mk*ceil(n/512) + kn*ceil(m/256) input elements, C once in and once out), its HBM bytes lie between the
+    compulsory bytes and everything the tiles read."""
+    m, n, k = 2048, 3072, 1024
+    hier = T.CacheHierarchy.from_capacities([256 * 512, 232448, 132644864 // 2])
+    d = T.parse_name("C2A1C0")
+    bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(256, 512)),
+                             pinned=T.BlocksizeSet({(1, "m"): 256, (2, "m"): 1024, (2, "n"): 1024}))
+    nest = T.build_plan(d, bs, hier, T.Shape(m, n, k))
+    g = nest.gpu_model_tc(dtype, T.ExecOptions(tile=256, tile_n=512), sms=148)
+    tiles = (m // 256) * (n // 512)
+    assert g["tile"] == (256, 512) and g["tasks"] == tiles and g["grid"] == min(74, tiles)
+    a_el = m * k * math.ceil(n / 512)
+    b_el = k * n * math.ceil(m / 256)
+    assert g["smem_elements"]["A"] == (a_el, 0) and g["smem_elements"]["B"] == (b_el, 0)
+    assert g["smem_elements"]["C"] == (m * n, m * n)
+    assert g["smem_bytes"] == eb * (a_el + b_el) + 4 * 2 * m * n
+    compulsory = eb * (m * k + k * n) + 4 * m * n
+    assert compulsory <= g["hbm_read_bytes"] <= eb * (a_el + b_el) + 4 * m * n
+    assert g["hbm_bytes"]["C"][1] == 4 * m * n  # C written back once
