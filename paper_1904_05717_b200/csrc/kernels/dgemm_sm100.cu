@@ -666,6 +666,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
 
     for (; ti < t_hi; ti += t_step) {
         const Task t = a.tasks[ti];
+        // last task of this CTA: let a programmatically dependent launch (the next segment of the task list)
+        // start its CTAs as this launch's CTAs retire, instead of after the slowest one
+        if (a.pdl_trigger && ti + t_step >= t_hi) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
         wait_ready(a, t);
         wait_turn(a, t);
         const int nk = (t.k + BK - 1) / BK;
@@ -985,7 +988,7 @@ cudaError_t launch(Kernel kernel, bool vec16, const Args& args, int grid, cudaSt
 int tma_bk(Kernel kernel) { return kernel >= 0 && kernel < kKernelCount ? kTmaTable[kernel].bk : 0; }
 
 cudaError_t launch_tma(Kernel kernel, const Args& args, int64_t M, int64_t N, int64_t K, int grid,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, bool pdl) {
     if (kernel < 0 || kernel >= kKernelCount || kTmaTable[kernel].fn == nullptr) return cudaErrorNotSupported;
     const TmaEntry& en = kTmaTable[kernel];
     if ((args.lda & 1) || (args.ldb & 1) || (reinterpret_cast<uintptr_t>(args.A) & 15) ||
@@ -1048,8 +1051,23 @@ cudaError_t launch_tma(Kernel kernel, const Args& args, int64_t M, int64_t N, in
         return env ? std::atoi(env) : 1;
     }();
     local.prefetch_c &= prefetch_knob;
+    local.pdl_trigger = 1;  // (harmless without a dependent launch)
+    if (!pdl) {
+        void* params[] = {&local, &ma, &mb, &mc};
+        return cudaLaunchKernel(en.fn, dim3(grid), dim3(kTable[kernel].threads), params, en.smem, stream);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(kTable[kernel].threads));
+    cfg.dynamicSmemBytes = static_cast<size_t>(en.smem);
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
     void* params[] = {&local, &ma, &mb, &mc};
-    return cudaLaunchKernel(en.fn, dim3(grid), dim3(kTable[kernel].threads), params, en.smem, stream);
+    return cudaLaunchKernelExC(&cfg, en.fn, params);
 }
 
 cudaError_t launch_reduce_tiles(double* C, int64_t ldc, const double* work, int64_t work_ld, int64_t work_slice,

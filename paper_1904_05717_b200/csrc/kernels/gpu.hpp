@@ -55,6 +55,7 @@ struct Args {
     const int32_t* ready;      // data flags written by the copy stream (Task::ready), or nullptr
     int32_t* done;             // per-block completion counters (Task::done), or nullptr
     int32_t prefetch_c = 0;    // TMA kernels: warm L2 with each task's C tile when the producer reaches it
+    int32_t pdl_trigger = 0;   // TMA kernels: griddepcontrol.launch_dependents at each CTA's last task
 };
 
 // One k-split C tile: its partials live in slots slot0 .. slot0+nslots-1 and
@@ -95,8 +96,10 @@ cudaError_t launch(Kernel kernel, bool vec16, const Args& args, int grid, cudaSt
 // ends at K (out-of-range rows/columns are zero-filled by the TMA unit).
 // cudaErrorNotSupported: no TMA variant, unaligned operands, or lower
 // occupancy than the cp.async kernel the grid was sized for.
+// pdl: programmatic dependent launch after the previous kernel on the stream (a later segment of the same
+// task list): its CTAs may start as the previous launch's CTAs retire (they trigger at their last task).
 cudaError_t launch_tma(Kernel kernel, const Args& args, int64_t M, int64_t N, int64_t K, int grid,
-                       cudaStream_t stream);
+                       cudaStream_t stream, bool pdl = false);
 int tma_bk(Kernel kernel);  // k-slab depth of the TMA variant (0 = none)
 // cuTensorMapEncodeTiled from the driver (nullptr if unavailable).
 void* tensor_map_encoder();

@@ -534,7 +534,15 @@ int launch_tasks(Schedule& s, const gpu::Args& a, int64_t M, int64_t N, int64_t 
             gpu::Args sa = a;
             sa.tasks = a.tasks + s.segments[q];
             sa.ntasks = s.segments[q + 1] - s.segments[q];
-            const cudaError_t r = gpu::launch_tma(s.kernel, sa, M, N, K, std::min(s.grid, sa.ntasks), stream);
+            static const int pdl_knob = [] {  // TILEMUL_TMA_PDL=0: A/B knob
+                const char* env = std::getenv("TILEMUL_TMA_PDL");
+                return env ? std::atoi(env) : 1;
+            }();
+            // segments after the first start their CTAs as the previous segment's CTAs retire (programmatic
+            // dependent launch): the segments' tasks are distinct C tiles, and split parts straddling a
+            // segment boundary synchronise through the fix-up counters, never through launch order
+            const cudaError_t r = gpu::launch_tma(s.kernel, sa, M, N, K, std::min(s.grid, sa.ntasks), stream,
+                                                  q > 0 && pdl_knob);
             if (r == cudaErrorNotSupported && q == 0) ok = false;  // (decided before any launch)
             else cuda_check(r, "task kernel launch (TMA segment)");
         }
