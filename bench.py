@@ -559,8 +559,11 @@ def tc_arm(args):
     # under the power cap, which this step count does not reach)
     if dtype == "bf16" and peaks.get("bf16_tflops"):
         peak, src = peaks["bf16_tflops"], "MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3 burst)"
-    elif dtype == "tf32" and peaks.get("bf16_tflops"):
-        peak, src = peaks["bf16_tflops"] / 2, "MEASURED_PEAKS.json bf16_tflops / 2 (tf32 issues at half the bf16 rate)"
+    elif dtype == "tf32":
+        # MEASURED_PEAKS.json has no tf32 figure: the live tcgen05 tf32 issue-rate probe, which measures the
+        # nominal dense 1.1 PFLOP/s of B200_PROFILING.md at full clock (cuBLAS's bf16 burst / 2 would sit below
+        # what the kernel reaches)
+        peak, src = probe, "tcgen05 tf32 issue-rate probe (live, full clock; nominal 1.1 PFLOP/s dense)"
     else:
         peak, src = probe, "tcgen05 issue-rate probe (live)"
     workload = workload_name(m, n, k, family, dtype)
