@@ -247,3 +247,40 @@ def test_tma_long_launch_auto_stays_cpasync():
     a2, b2, c2 = O.fill_uniform(78, [(m, 4096), (4096, n), (m, n)])
     _, st = run(nest2, torch.from_numpy(a2).cuda(), torch.from_numpy(b2).cuda(), c2, split_k=1)
     assert st == "tma"
+
+
+def test_segments_and_programmatic_launch_are_bitwise_invisible():
+    """A TMA task list longer than 4096 slabs per CTA runs in segments of whole rounds, the segments chained
+    by programmatic dependent launch (default) or plain stream order (TILEMUL_TMA_PDL=0); both give C
+    bitwise equal to the cp.async kernel in one launch: segmentation and launch chaining change when CTAs
+    start, never which tasks run or their k order. Knobs are read once per process: one child per setting."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, hashlib; sys.path.insert(0, %r)\n"
+            "import torch\n"
+            "from paper_1904_05717_b200 import tilemul as T, planner as P\n"
+            "m, n, k = 2048, 2048, 81920\n"
+            "nest, bs, hier = P.plan_for_gpu('C2A1C0', (m, n, k), 'fused')\n"
+            "A = torch.empty(m * k, dtype=torch.float64, device='cuda')\n"
+            "B = torch.empty(k * n, dtype=torch.float64, device='cuda')\n"
+            "C = torch.empty(m * n, dtype=torch.float64, device='cuda')\n"
+            "for x, s in ((A, 1), (B, 2), (C, 3)): T.fill_uniform_device(x, s)\n"
+            "T.execute(nest, A, B, C, T.ExecOptions(split_k=1, staging=sys.argv[1]))\n"
+            "torch.cuda.synchronize()\n"
+            "print(nest.last_launch()['launches'], nest.last_launch()['staging'],"
+            " hashlib.sha256(C.cpu().numpy().tobytes()).hexdigest())\n") % root
+    out = {}
+    for name, staging, env in (("segments, PDL", "auto", {}),
+                               ("segments, stream order", "auto", {"TILEMUL_TMA_PDL": "0"}),
+                               ("cp.async, one launch", "cpasync", {})):
+        r = subprocess.run([sys.executable, "-c", code, staging], env={**os.environ, **env}, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        launches, got_staging, digest = r.stdout.split()[-3:]
+        out[name] = (int(launches), got_staging, digest)
+    assert out["segments, PDL"][:2] == (2, "tma") and out["segments, stream order"][:2] == (2, "tma"), out
+    assert out["cp.async, one launch"][:2] == (1, "cpasync"), out
+    assert len({d for _, _, d in out.values()}) == 1, out
