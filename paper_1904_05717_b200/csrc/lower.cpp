@@ -152,7 +152,18 @@ HostSchedule plan_tasks(const Nest& nest, const tm_exec_opts& o, gpu::Kernel ker
         // Balances the machine exactly and staggers the tile boundaries
         // (C loads/stores) of different CTAs in time.
         const bool ragged = ntiles % slots != 0 && ntiles < 8 * slots && ntiles * 2 > slots;
-        if (dmma && (o.split_k == -1 || (o.split_k == 0 && ragged && e.k >= 2048))) {
+        // Round 2: auto also takes stream-K whenever the tiles do not fill whole waves and the launch is
+        // short (at most 4096 k-slabs per CTA: one TMA launch, no segments, which need whole rounds).
+        // Measured back to back against the per-tile / tail splits (profiles/ab_r02_streamk_auto.json):
+        // 512^2 x 131072 92.5 -> 95.2 %, 1024^2 x 65536 82.8 -> 96.1 %, rank-k 90.4 -> 91.5 %,
+        // 65536 x 256 x 1024 92.5 -> 93.2 %.
+        static const int sk_knob = [] {  // TILEMUL_STREAMK_AUTO=0: A/B knob
+            const char* env = std::getenv("TILEMUL_STREAMK_AUTO");
+            return env ? std::atoi(env) : 1;
+        }();
+        const i64 nks_all = cdiv(e.k, static_cast<i64>(32));
+        const bool short_uneven = sk_knob && ntiles % slots != 0 && ntiles * nks_all <= int64_t{4096} * slots;
+        if (dmma && (o.split_k == -1 || (o.split_k == 0 && ((ragged && e.k >= 2048) || short_uneven)))) {
             const i64 slab = 32, nks = cdiv(e.k, slab), U = ntiles * nks;
             const int G = static_cast<int>(std::min<i64>(slots, U));
             std::vector<std::vector<std::array<i64, 2>>> pieces(tiles.size());  // per tile: (slab_lo, slab_hi)
