@@ -79,3 +79,21 @@ def test_selects_gpu_mode_cheapest_member(shape, best):
     feasible = [c for c in ranked if c.blocksizes is not None]
     assert len(feasible) == len(P.GPU_MEMBERS)
     assert all(feasible[i].hbm_bytes <= feasible[i + 1].hbm_bytes for i in range(len(feasible) - 1))
+
+
+def test_tc_plan_uses_the_measured_raster_clipped_to_the_shape():
+    """Config 4's plan (planner.plan_tc_for_gpu): register tile = the SM pair's 256 x 512 TMEM accumulator,
+    SMEM-level m = 256, and the raster's L2 block pinned to the measured TC_L2_BLOCK, clipped to the shape;
+    the nest validates against the pair's hierarchy."""
+    from paper_1904_05717_b200 import planner as P
+    from paper_1904_05717_b200 import tilemul as T
+
+    nest, bs, hier = P.plan_tc_for_gpu("C2A1C0", (16384, 16384, 16384))
+    e = dict(bs.entries())
+    assert (e[(0, "m")], e[(0, "n")], e[(1, "m")]) == (256, 512, 256)
+    assert (e[(2, "m")], e[(2, "n")]) == P.TC_L2_BLOCK
+    assert (nest.m_r, nest.n_r) == (256, 512)
+    small, bs2, _ = P.plan_tc_for_gpu("C2A1C0", (1000, 776, 328))
+    e2 = dict(bs2.entries())
+    assert (e2[(2, "m")], e2[(2, "n")]) == (1000, 776)
+    assert small.shape == T.Shape(1000, 776, 328)
