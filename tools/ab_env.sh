@@ -19,6 +19,6 @@ for l in sys.stdin:
     d=json.loads(l); print(d.get('impl','ours'), d['dtype'], round(d['tflops'],1))"; fi
 for v in $VALS; do
   env $VAR=$v TC_CASES=${NCU_CASE:-bf16:256:512} TC_CUBLAS=0 timeout 400 ncu --clock-control none \
-    --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,sm__cycles_elapsed.avg.per_second \
-    -k regex:k_tc2 -s 3 -c 1 --csv timeout 300 python tools/bench_tc.py 2>/dev/null | grep -E '"(dram|gpu__time|sm__)' | awk -F'","' '{print "'$VAR'='$v' ncu "$(NF-2)" "$NF}'
+    --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active,sm__cycles_elapsed.avg.per_second,lts__t_sectors_srcunit_tex_op_read.sum,l1tex__m_xbar2l1tex_read_bytes.sum \
+    -k regex:k_tc2 -s 3 -c 1 --csv timeout 300 python tools/bench_tc.py 2>/dev/null | grep -E "\"(dram|gpu__time|sm__|lts__|l1tex__)" | awk -F'","' '{print "'$VAR'='$v' ncu "$(NF-2)" "$NF}'
 done
