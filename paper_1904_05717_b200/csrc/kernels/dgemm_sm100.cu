@@ -85,6 +85,30 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// ---- per-CTA timeline probe (experiment builds only: -DTM_TRACE) ----
+// Thread 0 stamps (globaltimer, clock64, event | task << 8) at task-boundary
+// events of k_dmma_tma; tm_trace_read copies them out. Off in the product build.
+#ifdef TM_TRACE
+constexpr int kTraceCtas = 160, kTraceEv = 1024;
+__device__ unsigned long long g_trace[kTraceCtas * kTraceEv * 3];
+__device__ int g_trace_n[kTraceCtas];
+__device__ __forceinline__ void trace_ev(int ev, int ti) {
+    if (threadIdx.x != 0 || blockIdx.x >= kTraceCtas) return;
+    const int i = g_trace_n[blockIdx.x]++;
+    if (i >= kTraceEv) return;
+    unsigned long long gt, ck;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(ck));
+    unsigned long long* p = g_trace + (static_cast<size_t>(blockIdx.x) * kTraceEv + i) * 3;
+    p[0] = gt;
+    p[1] = ck;
+    p[2] = static_cast<unsigned long long>(ev) | (static_cast<unsigned long long>(ti) << 8);
+}
+#define TM_TRACE_EV(ev, ti) trace_ev(ev, ti)
+#else
+#define TM_TRACE_EV(ev, ti) ((void)0)
+#endif
+
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c[0]), "+d"(c[1])
@@ -662,6 +686,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
         p_load(ti);
     }
     __syncwarp();
+    TM_TRACE_EV(0, 0);
 
 
     for (; ti < t_hi; ti += t_step) {
@@ -671,6 +696,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
         if (a.pdl_trigger && ti + t_step >= t_hi) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
         wait_ready(a, t);
         wait_turn(a, t);
+        TM_TRACE_EV(1, ti);
         const int nk = (t.k + BK - 1) / BK;
         if (warp == 0) top_up(n_use + PD, ti);
 
@@ -694,10 +720,14 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
                         acc[mi][ni][e] = (d.src && r + e < t.m && c < t.n) ? __ldcg(p + e) : 0.0;
                 }
             }
+        TM_TRACE_EV(2, ti);
 
         for (int s = 0; s < nk; ++s) {
             const uint32_t stage = n_use % STAGES;
             mbar_wait_warp(&full[stage], (n_use / STAGES) & 1);
+#ifdef TM_TRACE
+            if (s == 0) TM_TRACE_EV(3, ti);
+#endif
             const unsigned char* st = sgen + stage * STAGE_BYTES;
 #pragma unroll
             for (int kk = 0; kk < KK; ++kk) {
@@ -720,9 +750,11 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
             if (lane == 0) mbar_arrive(&empty[stage]);
             ++n_use;
         }
+        TM_TRACE_EV(4, ti);
         if constexpr (FIX) {
             if (t.fixup == 2) fold_partials<FM, FN, true>(a, t, acc, wm0, wn0, g, tq);
         }
+        TM_TRACE_EV(5, ti);
 
         const int64_t di = d.oi, dj = d.oj;
         const bool dst_vec = ((reinterpret_cast<uintptr_t>(d.dst) & 15) | (d.ld_dst & 1) | (di & 1)) == 0;
@@ -742,7 +774,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
             }
         if (FIX && t.fixup == 1) signal_partial(a, t);
         else signal_done(a, t, ti);
+        TM_TRACE_EV(6, ti);
     }
+    TM_TRACE_EV(7, 0);
 }
 
 // ============================== SIMT kernels =============================
@@ -1094,3 +1128,22 @@ cudaError_t launch_fill(double* x, int64_t count, uint64_t seed, uint64_t offset
 
 }  // namespace gpu
 }  // namespace mmm
+
+#ifdef TM_TRACE
+// Experiment builds only: copy the per-CTA timeline out and reset it.
+// out: ctas x events x 3 u64 (globaltimer ns, clock64, event | task << 8); counts: events per CTA.
+extern "C" __attribute__((visibility("default"))) int tm_trace_read(unsigned long long* out, int* counts) {
+    using namespace mmm::gpu;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 3;
+    if (cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * kTraceCtas * kTraceEv * 3) != cudaSuccess)
+        return 3;
+    if (cudaMemcpyFromSymbol(counts, g_trace_n, sizeof(int) * kTraceCtas) != cudaSuccess) return 3;
+    static int zero[kTraceCtas] = {};
+    return cudaMemcpyToSymbol(g_trace_n, zero, sizeof(zero)) == cudaSuccess ? 0 : 3;
+}
+extern "C" __attribute__((visibility("default"))) int tm_trace_dims(int* ctas, int* events) {
+    *ctas = mmm::gpu::kTraceCtas;
+    *events = mmm::gpu::kTraceEv;
+    return 0;
+}
+#endif
