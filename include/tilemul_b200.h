@@ -216,6 +216,14 @@ int tm_execute(tm_plan* plan, const double* A, int64_t lda, const double* B, int
  * A, B, C to the device, runs, copies C back; synchronous. Host memory may be
  * pinned (fast path) or pageable. */
 int tm_execute_host(tm_plan* plan, const double* A, const double* B, double* C, const tm_exec_opts* opts);
+/* The upload order tm_execute_host's copy-engine-fed pipeline uses for the plan's
+ * extents (host logic only, no device call): records of 6 int64, in issue
+ * order -- {1|2|3 = a piece of A|B|C, r0, rows, c0, cols, 0} for every upload,
+ * then {0, i0, i1, j0, j1, q} = the data flag written after them and the cell
+ * box (rows [i0,i1) x columns [j0,j1) of k-chunk q) whose tasks wait for it.
+ * *count = records in total (call with records = NULL to size the buffer).
+ * Pipelines apply when k >= 4096 or n >= 4096 (fused, unsplit). */
+int tm_host_pipe_steps(const tm_plan* plan, int64_t* records, int64_t cap, int64_t* count);
 /* Mixed precision on the 5th-generation tensor cores (tcgen05 + TMEM,
  * BASELINE configs[3]): C(m x n, fp32) += A·B with A, B column-major in BF16
  * (dtype TM_DTYPE_BF16) or in fp32 holding TF32 values (TM_DTYPE_TF32),

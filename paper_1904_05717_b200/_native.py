@@ -93,6 +93,7 @@ SIGNATURES = [
     ("tm_roofline_bound", dbl, [dbl, dbl, dbl]),
     ("tm_execute", C.c_int, [P, P, i64, P, i64, P, i64, C.POINTER(tm_exec_opts), P]),
     ("tm_execute_host", C.c_int, [P, P, P, P, C.POINTER(tm_exec_opts)]),
+    ("tm_host_pipe_steps", C.c_int, [P, C.POINTER(i64), i64, C.POINTER(i64)]),
     ("tm_execute_tc", C.c_int, [P, C.c_int, P, i64, P, i64, P, i64, C.POINTER(tm_exec_opts), P]),
     ("tm_round_inputs", C.c_int, [C.c_int, P, P, i64, P]),
     ("tm_layout_address", C.c_int, [i64, i64, C.POINTER(i32), C.POINTER(i64), C.c_int, i64, i64, C.POINTER(i64)]),

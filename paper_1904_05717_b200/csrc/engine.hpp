@@ -70,17 +70,31 @@ struct Key {
 // the download of a block waits on its completion counter.
 struct HostPipe {
     tm_exec_opts opts{};
-    std::vector<i64> kcut, ncut;
-    std::vector<std::pair<int, int>> units;  // (block, chunk) in issue order
-    std::vector<int32_t> block_tasks;        // tasks of each block's last unit
+    std::vector<i64> mcut, kcut, ncut;
+    // One upload step: its pieces go up on the copy stream, then the step's
+    // data flag is written; the tasks the step enables wait for that flag.
+    struct Piece {
+        char op;        // 'A', 'B' or 'C'
+        i64 r0, rows;   // row range of the operand (A: m, B: k, C: m)
+        i64 c0, cols;   // column range (A: k, B: n, C: n)
+    };
+    struct Step {
+        std::vector<Piece> pieces;
+        i64 i0 = 0, i1 = 0, j0 = 0, j1 = 0;  // the cell box the step enables: rows x columns ...
+        int q = 0;                           // ... of k-chunk q
+    };
+    std::vector<Step> steps;                 // in issue order
+    std::vector<int32_t> block_tasks;        // last-chunk tasks of each C column block
     std::unique_ptr<Schedule> sched;
-    int32_t* flags = nullptr;  // [units] data-ready flags, then [blocks] done counters
+    int32_t* flags = nullptr;  // [steps] data-ready flags, then [blocks] done counters
     int regions = 0;
     ~HostPipe() {
         if (flags) cudaFree(flags);
     }
 };
 
+// The pipeline's cuts and upload steps for extents e (pure host logic, no device calls).
+void pipe_order(const Extents& e, HostPipe& P);
 int sm_count();
 // Launch the schedule's task kernel: the TMA-fed DMMA variant when the
 // options allow and the operands/task list fit it, else the cp.async one.

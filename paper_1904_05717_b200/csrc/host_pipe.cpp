@@ -1,7 +1,7 @@
 // Host-buffer execution (tm_execute_host): copies in, the GEMM, C back,
-// pipelined. Preferred: one persistent launch over every (C column block,
-// k-chunk) unit, fed by the copy engine through stream memory operations;
-// fallback: one launch per unit.
+// pipelined. Preferred: one persistent launch over every (A row block, C
+// column block, k-chunk) cell, fed by the copy engine through stream memory
+// operations; fallback: one launch per (column block, k-chunk) unit.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -62,81 +62,131 @@ std::vector<i64> even_cuts(i64 total, int pieces, i64 align) {
     return start;
 }
 
-// Lowers every unit's sub-nest (fused, unsplit) and splices the task lists
-// into one, in unit order, with global coordinates; each task waits for its
-// unit's data flag and for the previous chunk of its C tile (progress
-// counters, as in the faithful schedule), so every C entry still sees its k
-// chunks in ascending order.
+// The upload order is a growing box over (A row blocks, C column blocks,
+// k-chunks): after the first block of each, the next extension is whichever
+// of a new A row block, a new C column block or a new k-chunk enables the
+// most GEMM work per element copied, and every piece of an extension is one
+// step with its own data flag. Each step's sub-nest is lowered (fused,
+// unsplit) and the task lists are spliced into one, in step order, with
+// global coordinates; a task waits for its step's flag and for the previous
+// chunk of its C tile (progress counters, as in the faithful schedule), so
+// every C entry still sees its k chunks in ascending order. Cutting A into
+// row blocks (round 2) lets the first GEMM start after ~100 MB instead of a
+// whole 512 MB k-chunk of A at 16384^3.
+}  // namespace
+
+void pipe_order(const Extents& e, HostPipe& P) {
+    // k-chunks of >= 4096 (at most 4) and column blocks of >= 256 (at most
+    // 64): at 16384^3 on PCIe Gen5 these measured best among 4..16 chunks x
+    // 8..64 blocks (tools/e2e_probe.py); smaller k-chunks cost more C round
+    // trips. Row blocks of A of >= 2048 (at most 8; TILEMUL_PIPE_ROWBLOCKS: A/B knob): 16 KB runs per
+    // column in their 2-D copies.
+    static const int row_knob = [] {
+        const char* env = std::getenv("TILEMUL_PIPE_ROWBLOCKS");
+        return env ? std::max(1, std::atoi(env)) : 8;
+    }();
+    P.kcut = even_cuts(e.k, static_cast<int>(std::max<i64>(1, std::min<i64>(4, e.k / 4096))), 32);
+    P.ncut = even_cuts(e.n, static_cast<int>(std::max<i64>(1, std::min<i64>(64, e.n / 256))), 128);
+    P.mcut = even_cuts(e.m, static_cast<int>(std::max<i64>(1, std::min<i64>(row_knob, e.m / 2048))), 128);
+    P.steps.clear();
+    const auto& mc = P.mcut;
+    const auto& nc = P.ncut;
+    const auto& kc = P.kcut;
+    const int NI = static_cast<int>(mc.size()) - 1, NJ = static_cast<int>(nc.size()) - 1,
+              NQ = static_cast<int>(kc.size()) - 1;
+    auto at = [](const std::vector<i64>& v, int x) { return v[static_cast<std::size_t>(x)]; };
+    auto a_piece = [&](int i, int q) {
+        return HostPipe::Piece{'A', at(mc, i), at(mc, i + 1) - at(mc, i), at(kc, q), at(kc, q + 1) - at(kc, q)};
+    };
+    auto b_piece = [&](int q, i64 j0, i64 j1) {
+        return HostPipe::Piece{'B', at(kc, q), at(kc, q + 1) - at(kc, q), j0, j1 - j0};
+    };
+    auto c_piece = [&](int j) { return HostPipe::Piece{'C', 0, e.m, at(nc, j), at(nc, j + 1) - at(nc, j)}; };
+    auto step = [&](std::vector<HostPipe::Piece> pieces, i64 i0, i64 i1, i64 j0, i64 j1, int q) {
+        HostPipe::Step s;
+        s.pieces = std::move(pieces);
+        s.i0 = i0, s.i1 = i1, s.j0 = j0, s.j1 = j1, s.q = q;
+        P.steps.push_back(std::move(s));
+    };
+    step({c_piece(0), a_piece(0, 0), b_piece(0, nc[0], nc[1])}, mc[0], mc[1], nc[0], nc[1], 0);
+    int ni = 1, nj = 1, nq = 1;
+    while (ni < NI || nj < NJ || nq < NQ) {
+        const double Mi = static_cast<double>(at(mc, ni)), Nj = static_cast<double>(at(nc, nj)),
+                     Kq = static_cast<double>(at(kc, nq)), M = static_cast<double>(e.m);
+        // GEMM work enabled per element copied. A C column block is copied whole (all M rows, contiguous):
+        // cutting C into row blocks too would enable work sooner per byte, but the short runs of its 2-D
+        // copies cost more than that gains (16384^3: 262.4 ms against 259.2 with 2048-row blocks, 280.2 with
+        // 1024-row blocks whose runs are 8 KB; profiles/ab_r02_pipe_rowblocks.json).
+        const double ri = ni < NI ? Nj : -1.0;
+        const double rj = nj < NJ ? Mi * Kq / (M + Kq) : -1.0;
+        const double rq = nq < NQ ? Mi * Nj / (Mi + Nj) : -1.0;
+        if (ri > rj && ri > rq) {  // a new row block of A, chunk by chunk
+            for (int q = 0; q < nq; ++q) step({a_piece(ni, q)}, at(mc, ni), at(mc, ni + 1), nc[0], at(nc, nj), q);
+            ++ni;
+        } else if (rq > rj) {  // a new k-chunk: its B rows for the loaded columns, then A row block by row block
+            for (int i = 0; i < ni; ++i) {
+                std::vector<HostPipe::Piece> pcs;
+                if (i == 0) pcs.push_back(b_piece(nq, nc[0], at(nc, nj)));
+                pcs.push_back(a_piece(i, nq));
+                step(std::move(pcs), at(mc, i), at(mc, i + 1), nc[0], at(nc, nj), nq);
+            }
+            ++nq;
+        } else {  // a new C column block with its B columns, chunk by chunk
+            for (int q = 0; q < nq; ++q) {
+                std::vector<HostPipe::Piece> pcs;
+                if (q == 0) pcs.push_back(c_piece(nj));
+                pcs.push_back(b_piece(q, at(nc, nj), at(nc, nj + 1)));
+                step(std::move(pcs), mc[0], at(mc, ni), at(nc, nj), at(nc, nj + 1), q);
+            }
+            ++nj;
+        }
+    }
+}
+
+namespace {
+
 std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o, cudaStream_t st) {
     const Extents& e = plan.nest.ext;
     auto P = std::make_unique<HostPipe>();
     P->opts = o;
-    // k-chunks of >= 4096 (at most 4) and column blocks of >= 256 (at most
-    // 64): at 16384^3 on PCIe Gen5 these measured best among 4..16 chunks x
-    // 8..64 blocks (tools/e2e_probe.py); smaller k-chunks cost more C round
-    // trips, larger first pieces delay the first GEMM.
-    P->kcut = even_cuts(e.k, static_cast<int>(std::max<i64>(1, std::min<i64>(4, e.k / 4096))), 32);
-    P->ncut = even_cuts(e.n, static_cast<int>(std::max<i64>(1, std::min<i64>(64, e.n / 256))), 128);
-    const int nq = static_cast<int>(P->kcut.size()) - 1, nbk = static_cast<int>(P->ncut.size()) - 1;
-    // Growing-rectangle order: after (A_0, C_0), load next whichever of the
-    // next A k-chunk or the next C column block enables more GEMM work per
-    // byte copied, then run the (block, chunk) units it enables: a new A
-    // chunk adds column q for every loaded block, a new C block adds row b
-    // for every loaded chunk (ascending q, so each C entry still sees its k
-    // chunks in order). Early on this keeps the copy stream ahead of the
-    // math instead of front-loading all of A.
-    {
-        int na = 1, nc = 1;
-        P->units.push_back({0, 0});
-        const double mm = static_cast<double>(e.m);
-        while (na < nq || nc < nbk) {
-            const double kq = static_cast<double>(na < nq ? P->kcut[static_cast<std::size_t>(na) + 1] - P->kcut[static_cast<std::size_t>(na)] : 1);
-            const double wb = static_cast<double>(nc < nbk ? P->ncut[static_cast<std::size_t>(nc) + 1] - P->ncut[static_cast<std::size_t>(nc)] : 1);
-            const double wavg = static_cast<double>(P->ncut[static_cast<std::size_t>(nc)]) / nc;   // loaded columns per block
-            const double kavg = static_cast<double>(P->kcut[static_cast<std::size_t>(na)]) / na;  // loaded k per chunk
-            // flops per byte of the copies each choice needs
-            const double ra = na < nq ? (nc * mm * kq * wavg) / (mm * kq + nc * kq * wavg) : -1.0;
-            const double rc = nc < nbk ? (na * mm * kavg * wb) / (mm * wb + na * kavg * wb) : -1.0;
-            if (ra > rc) {
-                for (int b2 = 0; b2 < nc; ++b2) P->units.push_back({b2, na});
-                ++na;
-            } else {
-                for (int q2 = 0; q2 < na; ++q2) P->units.push_back({nc, q2});
-                ++nc;
-            }
-        }
-    }
+    pipe_order(e, *P);
+    const auto& nc = P->ncut;
+    const auto& kc = P->kcut;
+    const int NJ = static_cast<int>(nc.size()) - 1, NQ = static_cast<int>(kc.size()) - 1;
     tm_exec_opts uo = o;
     uo.split_k = 1;
     Nest first = plan.nest;
-    first.ext.n = P->ncut[1];
-    first.ext.k = P->kcut[1];
+    first.ext.m = P->mcut[1];
+    first.ext.n = nc[1];
+    first.ext.k = kc[1];
     const gpu::Kernel kernel = pick_kernel(first, uo, uo.staging != TM_STAGING_CPASYNC && e.m % 2 == 0 && e.k % 2 == 0);
     gpu::KernelInfo info{};
     cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
     const i64 mt = cdiv(e.m, info.tile_m);
     P->regions = static_cast<int>(mt * cdiv(e.n, info.tile_n));
-    P->block_tasks.assign(static_cast<std::size_t>(nbk), 0);
+    P->block_tasks.assign(static_cast<std::size_t>(NJ), 0);
     auto sched = std::make_unique<Schedule>();
     sched->kernel = kernel;
     auto& T = sched->host_tasks;
-    for (std::size_t u = 0; u < P->units.size(); ++u) {
-        const auto [b, q] = P->units[u];
-        const i64 j0 = P->ncut[static_cast<std::size_t>(b)], p0 = P->kcut[static_cast<std::size_t>(q)];
+    for (std::size_t u = 0; u < P->steps.size(); ++u) {
+        const HostPipe::Step& sp = P->steps[u];
         Nest sn = plan.nest;
-        sn.ext.n = P->ncut[static_cast<std::size_t>(b) + 1] - j0;
-        sn.ext.k = P->kcut[static_cast<std::size_t>(q) + 1] - p0;
+        sn.ext.m = sp.i1 - sp.i0;
+        sn.ext.n = sp.j1 - sp.j0;
+        sn.ext.k = kc[static_cast<std::size_t>(sp.q) + 1] - kc[static_cast<std::size_t>(sp.q)];
         const auto part = lower(sn, uo, kernel, st, false);
         for (gpu::Task tk : part->host_tasks) {
-            tk.j0 += static_cast<int32_t>(j0);
-            tk.p0 += static_cast<int32_t>(p0);
+            tk.i0 += static_cast<int32_t>(sp.i0);
+            tk.j0 += static_cast<int32_t>(sp.j0);
+            tk.p0 += static_cast<int32_t>(kc[static_cast<std::size_t>(sp.q)]);
             tk.tile = static_cast<int32_t>(tk.i0 / info.tile_m + (tk.j0 / info.tile_n) * mt);
-            tk.seq = q;
+            tk.seq = sp.q;
             tk.ready = static_cast<int32_t>(u) + 1;
-            tk.done = q == nq - 1 ? b + 1 : 0;
+            const int b = static_cast<int>(std::upper_bound(nc.begin(), nc.end(), static_cast<i64>(tk.j0)) - nc.begin()) - 1;
+            tk.done = sp.q == NQ - 1 ? b + 1 : 0;
+            if (sp.q == NQ - 1) ++P->block_tasks[static_cast<std::size_t>(b)];
             T.push_back(tk);
         }
-        if (q == nq - 1) P->block_tasks[static_cast<std::size_t>(b)] = static_cast<int32_t>(part->host_tasks.size());
     }
     if (T.size() > static_cast<std::size_t>(INT32_MAX)) fail_usage("too many tasks");
     sched->grid = std::max(1, std::min<int>(sm_count() * std::max(1, info.ctas_per_sm), static_cast<int>(T.size())));
@@ -146,7 +196,7 @@ std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o,
     cuda_check(cudaMalloc(&sched->tasks, sizeof(gpu::Task) * T.size()), "cudaMalloc(tasks)");
     cuda_check(cudaMemcpyAsync(sched->tasks, T.data(), sizeof(gpu::Task) * T.size(), cudaMemcpyHostToDevice, st),
                "upload tasks");
-    cuda_check(cudaMalloc(&P->flags, sizeof(int32_t) * (P->units.size() + static_cast<std::size_t>(nbk))),
+    cuda_check(cudaMalloc(&P->flags, sizeof(int32_t) * (P->steps.size() + static_cast<std::size_t>(NJ))),
                "cudaMalloc(pipeline flags)");
     cuda_check(cudaStreamSynchronize(st), "upload tasks (sync)");
     P->sched = std::move(sched);
@@ -168,7 +218,7 @@ void run_pipe(tm_plan* plan, const double* A, const double* B, double* C, const 
         plan->pipe = build_pipe(*plan, o, st);
     HostPipe& P = *plan->pipe;
     Schedule& S = *P.sched;
-    const std::size_t nu = P.units.size(), nbk = P.ncut.size() - 1;
+    const std::size_t nu = P.steps.size(), nbk = P.ncut.size() - 1;
     if (plan->chunk_ready.empty()) {
         cudaEvent_t ev;
         cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
@@ -185,28 +235,22 @@ void run_pipe(tm_plan* plan, const double* A, const double* B, double* C, const 
     // here (e2e 33.2 vs 32.8 TF/s at 16384^3); the HBM-traffic rule is the device path's
     plan->last_staging = launch_tasks(S, a, e.m, e.n, e.k, vec16, o.staging, st, true);
 
-    // uploads in first-need order, a flag after each unit's pieces
-    const std::size_t ldb = static_cast<std::size_t>(e.k) * sizeof(double);
+    // uploads in first-need order, a flag after each step's pieces
     cuda_check(cudaStreamWaitEvent(cs, zero, 0), "wait flags reset");
-    std::vector<char> have_a(P.kcut.size(), 0);
     for (std::size_t u = 0; u < nu; ++u) {
-        const auto [b, q] = P.units[u];
-        const i64 j0 = P.ncut[static_cast<std::size_t>(b)], w = P.ncut[static_cast<std::size_t>(b) + 1] - j0;
-        const i64 p0 = P.kcut[static_cast<std::size_t>(q)], kq = P.kcut[static_cast<std::size_t>(q) + 1] - p0;
-        if (q == 0)
-            cuda_check(cudaMemcpyAsync(plan->dC + j0 * e.m, C + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
-                                       cudaMemcpyHostToDevice, cs),
-                       "H2D C block");
-        if (!have_a[static_cast<std::size_t>(q)]) {
-            have_a[static_cast<std::size_t>(q)] = 1;
-            cuda_check(cudaMemcpyAsync(plan->dA + p0 * e.m, A + p0 * e.m, static_cast<std::size_t>(kq * e.m) * 8,
-                                       cudaMemcpyHostToDevice, cs),
-                       "H2D A chunk");
+        for (const HostPipe::Piece& pc : P.steps[u].pieces) {
+            const i64 ld = pc.op == 'B' ? e.k : e.m;  // leading dimension of the operand (host and device alike)
+            const double* src = (pc.op == 'A' ? A : pc.op == 'B' ? B : C) + pc.r0 + pc.c0 * ld;
+            double* dst = (pc.op == 'A' ? plan->dA : pc.op == 'B' ? plan->dB : plan->dC) + pc.r0 + pc.c0 * ld;
+            if (pc.rows == ld)
+                cuda_check(cudaMemcpyAsync(dst, src, static_cast<std::size_t>(pc.rows * pc.cols) * 8, cudaMemcpyHostToDevice, cs),
+                           "H2D piece");
+            else
+                cuda_check(cudaMemcpy2DAsync(dst, static_cast<std::size_t>(ld) * 8, src, static_cast<std::size_t>(ld) * 8,
+                                             static_cast<std::size_t>(pc.rows) * 8, static_cast<std::size_t>(pc.cols),
+                                             cudaMemcpyHostToDevice, cs),
+                           "H2D piece (2-D)");
         }
-        cuda_check(cudaMemcpy2DAsync(plan->dB + p0 + j0 * e.k, ldb, B + p0 + j0 * e.k, ldb,
-                                     static_cast<std::size_t>(kq) * 8, static_cast<std::size_t>(w),
-                                     cudaMemcpyHostToDevice, cs),
-                   "H2D B piece");
         cu_check(memops().write(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(P.flags + u), 1, 0),
                  "cuStreamWriteValue32");
     }

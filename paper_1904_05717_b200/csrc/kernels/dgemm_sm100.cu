@@ -115,8 +115,17 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+// Barrier over the CTA's task-running threads: all of them (__syncthreads), or, in kernels with an extra
+// producer warp behind them, the first NC threads (named barrier 1).
+template <int NC>
+__device__ __forceinline__ void cta_sync() {
+    if constexpr (NC == 0) __syncthreads();
+    else asm volatile("bar.sync 1, %0;\n" ::"n"(NC) : "memory");
+}
+
 // ---- ordering between tasks on the same C region (faithful schedule) ----
 // (fix-up tasks carry tile = -2 - counter, so this protocol skips them)
+template <int NC = 0>
 __device__ __forceinline__ void wait_turn(const Args& a, const Task& t) {
     if (t.tile < 0 || t.seq <= 0) return;
     if (threadIdx.x == 0) {
@@ -127,12 +136,13 @@ __device__ __forceinline__ void wait_turn(const Args& a, const Task& t) {
             __nanosleep(100);
         }
     }
-    __syncthreads();
+    cta_sync<NC>();
 }
 
+template <int NC = 0>
 __device__ __forceinline__ void signal_done(const Args& a, const Task& t, int ti) {
     if (t.tile < 0) return;
-    __syncthreads();
+    cta_sync<NC>();
     if (threadIdx.x == 0) {
         __threadfence();
         asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(a.progress + t.tile), "r"(t.seq + 1) : "memory");
@@ -145,6 +155,7 @@ __device__ __forceinline__ void signal_done(const Args& a, const Task& t, int ti
 
 // Copy-engine-fed pipeline: the task's inputs are in HBM once the copy stream
 // has written its flag (cuStreamWriteValue32 after the copies, in order).
+template <int NC = 0>
 __device__ __forceinline__ void wait_ready(const Args& a, const Task& t) {
     if (t.ready == 0) return;
     if (threadIdx.x == 0) {
@@ -156,15 +167,16 @@ __device__ __forceinline__ void wait_ready(const Args& a, const Task& t) {
             __nanosleep(256);
         }
     }
-    __syncthreads();
+    cta_sync<NC>();
 }
 
 // Split-k fix-up inside the task kernel (Task::fixup). Contributors publish
 // their partial with a release increment of the tile's counter; the owner
 // acquires the count, then adds the partials in slot order -- the same sums
 // in the same order as k_reduce_tiles, one launch and one C round trip less.
+template <int NC = 0>
 __device__ __forceinline__ void signal_partial(const Args& a, const Task& t) {
-    __syncthreads();
+    cta_sync<NC>();
     if (threadIdx.x == 0) {
         __threadfence();
         asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.progress + (-2 - t.tile)) : "memory");
@@ -197,7 +209,7 @@ __device__ __forceinline__ int c_col(int wn0, int ni, int g) {
         return wn0 + ni * 8 + g;
 }
 
-template <int FM, int FN, bool SWZ = false>
+template <int FM, int FN, bool SWZ = false, int NC = 0>
 __device__ __forceinline__ void fold_partials(const Args& a, const Task& t, double (&acc)[FM][FN][2], int wm0,
                                               int wn0, int g, int tq) {
     if (threadIdx.x == 0) {
@@ -210,7 +222,7 @@ __device__ __forceinline__ void fold_partials(const Args& a, const Task& t, doub
         }
         *ctr = 0;  // every contribution is in: ready for the next launch
     }
-    __syncthreads();
+    cta_sync<NC>();
     for (int q = 0; q < t.seq; ++q) {
         const double* w = a.work + static_cast<int64_t>(t.slice + q) * a.work_slice;
 #pragma unroll
@@ -571,6 +583,24 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
 #ifndef TM_TMA_ISSUE_KK
 #define TM_TMA_ISSUE_KK 2
 #endif
+// Experiment knobs (tools/build_variant.sh; the product build leaves them at their defaults): the k-slab depth
+// and stage count of the 128x128 TMA kernel, and a start-up stagger of its warp groups (warps w, w+4, w+8,
+// w+12 share an SM sub-partition; group w/4 starts (NW/4-1 - w/4) * TM_STAGGER cycles late, so the producer's
+// warp 0 trails and the groups reach the task boundaries' C exchange one after the other).
+#ifndef TM_TMA_BK128
+#define TM_TMA_BK128 32
+#endif
+#ifndef TM_TMA_ST128
+#define TM_TMA_ST128 3
+#endif
+#ifndef TM_STAGGER
+#define TM_STAGGER 0
+#endif
+// TM_PRODUCER_WARP = 1: the 128x128 TMA kernel runs a 17th warp that only issues the TMA copies (the 16
+// DMMA warps then fit 120 registers each), instead of warp 0's lane 0 issuing them between its own DMMAs.
+#ifndef TM_PRODUCER_WARP
+#define TM_PRODUCER_WARP 0
+#endif
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
                  : "memory");
@@ -583,11 +613,12 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, uin
         : "memory");
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool FIX = true>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool FIX = true, bool PW = false>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + (PW ? 32 : 0), 1)
     k_dmma_tma(Args a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC) {
     constexpr int NWM = BM / WM, NW = (BM / WM) * (BN / WN);
+    constexpr int NC = PW ? NW * 32 : 0;  // threads behind the task-boundary barriers (cta_sync)
     constexpr int FM = WM / 8, FN = WN / 8, KK = BK / 4;
     constexpr int PD = STAGES - 1;
     constexpr int ISSUE_KK = TM_TMA_ISSUE_KK < KK - 1 ? TM_TMA_ISSUE_KK : KK - 1;  // k step of the refill
@@ -681,24 +712,76 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
         }
         __syncwarp();
     };
-    if (threadIdx.x == 0) {
-        pc.issued = 0;
-        p_load(ti);
+    if constexpr (PW) {
+        // The producer warp: lane 0 walks the CTA's task list and keeps every stage of the ring filled, held
+        // back only by the stages' empty barriers (and a task's copy-engine data flag); then the warp exits.
+        if (warp == NW) {
+            if (lane == 0) {
+                uint32_t n = 0;
+                for (int x = ti; x < t_hi; x += t_step) {
+                    const Task pt = a.tasks[x];
+                    if (pt.k <= 0) continue;
+                    if (pt.ready != 0) {
+                        const int32_t* f = a.ready + pt.ready - 1;
+                        int v;
+                        for (;;) {
+                            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+                            if (v != 0) break;
+                            __nanosleep(256);
+                        }
+                    }
+                    if (a.prefetch_c && pt.slice < 0 && pt.ready == 0 && n > 0)
+                        asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                                         reinterpret_cast<uint64_t>(&tmC)),
+                                     "r"(pt.i0), "r"(pt.j0)
+                                     : "memory");
+                    const int pnk = (pt.k + BK - 1) / BK;
+                    for (int sl = 0; sl < pnk; ++sl, ++n) {
+                        const uint32_t stage = n % STAGES;
+                        if (n >= STAGES) mbar_wait(&empty[stage], ((n / STAGES) - 1) & 1);
+                        mbar_expect_tx(&full[stage], STAGE_BYTES);
+                        const uint32_t sa = sbase + stage * STAGE_BYTES;
+                        const int kc = pt.p0 + sl * BK;
+#pragma unroll
+                        for (int c = 0; c < BM / 16; ++c) tma_2d(sa + c * A_CHUNK, &tmA, &full[stage], pt.i0 + 16 * c, kc);
+#pragma unroll
+                        for (int c = 0; c < BK / 16; ++c)
+                            tma_2d(sa + A_BYTES + c * B_CHUNK, &tmB, &full[stage], kc + 16 * c, pt.j0);
+                    }
+                }
+            }
+            return;
+        }
+    } else {
+        if (threadIdx.x == 0) {
+            pc.issued = 0;
+            p_load(ti);
+        }
+        __syncwarp();
     }
-    __syncwarp();
     TM_TRACE_EV(0, 0);
-
+    [[maybe_unused]] bool restagger = true;
 
     for (; ti < t_hi; ti += t_step) {
         const Task t = a.tasks[ti];
         // last task of this CTA: let a programmatically dependent launch (the next segment of the task list)
         // start its CTAs as this launch's CTAs retire, instead of after the slowest one
         if (a.pdl_trigger && ti + t_step >= t_hi) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-        wait_ready(a, t);
-        wait_turn(a, t);
+        wait_ready<NC>(a, t);
+        wait_turn<NC>(a, t);
         TM_TRACE_EV(1, ti);
         const int nk = (t.k + BK - 1) / BK;
-        if (warp == 0) top_up(n_use + PD, ti);
+        if constexpr (!PW) {
+            if (warp == 0) top_up(n_use + PD, ti);
+        }
+        if constexpr (TM_STAGGER > 0 && NW >= 8) {
+            if (restagger) {  // (again after a task whose fix-up brought the CTA's warps back in step)
+                const long long t0 = clock64(), wait = static_cast<long long>(NW / 4 - 1 - (warp >> 2)) * TM_STAGGER;
+                while (clock64() - t0 < wait) {}
+                restagger = false;
+            }
+            if (FIX && t.fixup != 0) restagger = true;
+        }
 
         const Dest d = resolve(a, t);
         double acc[FM][FN][2];
@@ -744,7 +827,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
                 for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
                     for (int ni = 0; ni < FN; ++ni) dmma884(acc[mi][ni], bf[ni], af[mi]);
-                if (kk == ISSUE_KK && warp == 0) top_up(n_use + PD + 1, ti);
+                if constexpr (!PW) {
+                    if (kk == ISSUE_KK && warp == 0) top_up(n_use + PD + 1, ti);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
@@ -752,7 +837,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
         }
         TM_TRACE_EV(4, ti);
         if constexpr (FIX) {
-            if (t.fixup == 2) fold_partials<FM, FN, true>(a, t, acc, wm0, wn0, g, tq);
+            if (t.fixup == 2) fold_partials<FM, FN, true, NC>(a, t, acc, wm0, wn0, g, tq);
         }
         TM_TRACE_EV(5, ti);
 
@@ -772,8 +857,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1)
                         if (r + e < t.m && c < t.n) p[e] = acc[mi][ni][e];
                 }
             }
-        if (FIX && t.fixup == 1) signal_partial(a, t);
-        else signal_done(a, t, ti);
+        if (FIX && t.fixup == 1) signal_partial<NC>(a, t);
+        else signal_done<NC>(a, t, ti);
         TM_TRACE_EV(6, ti);
     }
     TM_TRACE_EV(7, 0);
@@ -959,9 +1044,11 @@ constexpr int tma_smem() {
 struct TmaEntry {
     const void* fn;
     int bk, box_n, smem;
+    int extra_threads = 0;  // a producer warp behind the task-running warps
 };
 const TmaEntry kTmaTable[kKernelCount] = {
-    {(const void*)k_dmma_tma<128, 128, kBKBig, 32, 32, kStagesBig>, kBKBig, 128, tma_smem<128, 128, kBKBig, kStagesBig>()},
+    {(const void*)k_dmma_tma<128, 128, TM_TMA_BK128, 32, 32, TM_TMA_ST128, true, TM_PRODUCER_WARP != 0>, TM_TMA_BK128, 128,
+     tma_smem<128, 128, TM_TMA_BK128, TM_TMA_ST128>(), TM_PRODUCER_WARP != 0 ? 32 : 0},
     {(const void*)k_dmma_tma<64, 64, kBKSmall, 32, 32, kStagesSmall>, kBKSmall, 64, tma_smem<64, 64, kBKSmall, kStagesSmall>()},
     {nullptr, 0, 0, 0},
     {nullptr, 0, 0, 0},
@@ -1036,7 +1123,7 @@ cudaError_t launch_tma(Kernel kernel, const Args& args, int64_t M, int64_t N, in
             if ((e = cudaFuncSetAttribute(en.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, en.smem)) != cudaSuccess)
                 return e;
             int occ = 0;
-            if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, en.fn, kTable[kernel].threads, en.smem)) !=
+            if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, en.fn, kTable[kernel].threads + en.extra_threads, en.smem)) !=
                 cudaSuccess)
                 return e;
             g_tma_occ[kernel] = occ > 0 ? occ : -1;
@@ -1088,11 +1175,11 @@ cudaError_t launch_tma(Kernel kernel, const Args& args, int64_t M, int64_t N, in
     local.pdl_trigger = 1;  // (harmless without a dependent launch)
     if (!pdl) {
         void* params[] = {&local, &ma, &mb, &mc};
-        return cudaLaunchKernel(en.fn, dim3(grid), dim3(kTable[kernel].threads), params, en.smem, stream);
+        return cudaLaunchKernel(en.fn, dim3(grid), dim3(kTable[kernel].threads + en.extra_threads), params, en.smem, stream);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
-    cfg.blockDim = dim3(static_cast<unsigned>(kTable[kernel].threads));
+    cfg.blockDim = dim3(static_cast<unsigned>(kTable[kernel].threads + en.extra_threads));
     cfg.dynamicSmemBytes = static_cast<size_t>(en.smem);
     cfg.stream = stream;
     cudaLaunchAttribute at[1];

@@ -632,6 +632,25 @@ class LoopNest:  # plan.hpp:25-85
         ranges = None if first[0] == -1 else list(first)
         return ts, grid.value, ranges
 
+    def host_pipe_steps(self) -> List[Dict]:
+        """The upload order of the host-buffer pipeline (tm_execute_host) for this
+        nest's extents: one dict per data flag, {"pieces": [(op, r0, rows, c0,
+        cols), ...], "box": (i0, i1, j0, j1), "chunk": q} -- the pieces copied
+        before the flag and the cells whose tasks wait for it (host logic only)."""
+        cnt = C.c_int64(0)
+        _check(N.lib().tm_host_pipe_steps(self._ptr, None, 0, C.byref(cnt)))
+        buf = (C.c_int64 * (6 * max(1, cnt.value)))()
+        _check(N.lib().tm_host_pipe_steps(self._ptr, buf, cnt.value, C.byref(cnt)))
+        steps, pieces = [], []
+        for r in range(cnt.value):
+            kind, a, b, c, d, e = buf[6 * r:6 * r + 6]
+            if kind == 0:
+                steps.append({"pieces": pieces, "box": (a, b, c, d), "chunk": e})
+                pieces = []
+            else:
+                pieces.append(("?ABC"[kind], a, b, c, d))
+        return steps
+
     def last_launch(self) -> Dict[str, int]:
         t, l, c = C.c_int64(0), C.c_int32(0), C.c_int32(0)
         _check(N.lib().tm_plan_last_launch(self._ptr, C.byref(t), C.byref(l), C.byref(c)))

@@ -217,9 +217,14 @@ def test_large_shapes_sampled_entries(shape, name, split):
 
 # --- host-buffer path (the reference's calling convention): the k-chunked
 # copy/compute pipeline gives bitwise the device-path result -----------------
-@pytest.mark.parametrize("numerics", ["dmma", "exact"])
-def test_host_buffer_pipeline_matches_device_path(numerics):
-    m, n, k = 520, 2200, 8224  # 2 k-chunks of 4128 / 4096, 8 column blocks of 384 (tail 296)
+@pytest.mark.parametrize("numerics,shape", [("dmma", (520, 2200, 8224)), ("exact", (520, 2200, 8224)),
+                                            ("dmma", (4200, 640, 8224)), ("exact", (4200, 640, 8224)),
+                                            ("dmma", (6200, 1100, 12320))])
+def test_host_buffer_pipeline_matches_device_path(numerics, shape):
+    # 520 x 2200 x 8224: 2 k-chunks of 4128 / 4096, 8 column blocks of 384 (tail 296), one row block;
+    # 4200 x 640 x 8224: 2 row blocks of A (2176 / 2024) x 2 column blocks x 2 k-chunks;
+    # 6200 x 1100 x 12320: 3 row blocks x 4 column blocks x 3 k-chunks (every extension kind of the growing box)
+    m, n, k = shape
     hier = T.gpu_hierarchy(128)
     d = T.parse_name("C2A1C0")
     bs = T.derive_blocksizes(d, hier, T.Shape(m, n, k), opts=T.DeriveOptions(micro=T.MicroTile(128, 128)),
@@ -232,7 +237,7 @@ def test_host_buffer_pipeline_matches_device_path(numerics):
     # one persistent launch over every (column block, k-chunk) unit, fed by the copy engine
     assert nest.last_launch()["tasks"] > 8  # (1 launch; one per unit under CUDA_LAUNCH_BLOCKING / profilers)
     assert np.array_equal(host_c.view(np.uint64), dev_out.view(np.uint64))
-    if numerics == "exact":
+    if numerics == "exact" and m * n * k < 2 ** 34:  # (the larger shapes: the device path is pinned to the oracle elsewhere)
         want = c.copy()
         O.execute_nest(m, n, k, [(L.dim, L.blocksize) for L in nest.loops], nest.m_r, nest.n_r, a, b, want)
         assert np.array_equal(host_c.view(np.uint64), want.view(np.uint64))
