@@ -416,7 +416,7 @@ def fp64_arm(args):
     launches_per_step = nest.last_launch()["launches"]
     staging = nest.last_launch()["staging"]
     tile = "128x128"
-    kernel_name = ("k_dmma_tma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3> (16 warps, TMA 128B-swizzled slabs"
+    kernel_name = ("k_dmma_tma<BM=128,BN=128,BK=32,WM=32,WN=32,stages=3> (16 DMMA warps + a producer warpgroup, TMA 128B-swizzled slabs"
                    + (f"; {launches_per_step} launches per step, segments of whole rounds" if launches_per_step > 1
                       else "") + ")" if staging == "tma" else
                    f"k_dmma (cp.async staging, {launches_per_step} launch(es) per step)")

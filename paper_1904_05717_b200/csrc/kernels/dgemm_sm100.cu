@@ -68,6 +68,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
 }
+// The same with an address operand `dep` (always 0) added: the instruction then waits for whatever produced dep.
+__device__ __forceinline__ void mbar_arrive_after(uint64_t* bar, uint32_t dep) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar) + dep) : "memory");
+}
 // Warp-uniform wait: lane 0 polls, __syncwarp hands its acquire to the
 // other lanes. (Every lane polling lets a warp split on the loop branch; the
 // lanes then issue their half of a coalesced cp.async separately, and the
@@ -596,10 +600,16 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
 #ifndef TM_STAGGER
 #define TM_STAGGER 0
 #endif
-// TM_PRODUCER_WARP = 1: the 128x128 TMA kernel runs a 17th warp that only issues the TMA copies (the 16
-// DMMA warps then fit 120 registers each), instead of warp 0's lane 0 issuing them between its own DMMAs.
+// TM_PRODUCER_WARP (default 1; 0 = the round-1/2 arrangement, an A/B knob): the 128x128 TMA kernel runs a
+// fifth warpgroup whose first lane only issues the TMA copies, instead of warp 0's lane 0 issuing them between
+// its own DMMAs (that warp then trailed the other fifteen, and every slab waited for it). The register file
+// is per SM sub-partition (16384 registers), so five warps there start at 96 registers each; the producer
+// warps then drop to 24 (setmaxnreg.dec) and the DMMA warps grow to 112: the pool setmaxnreg draws on is what
+// the CTA's own warps released (16 x 112 + 4 x 24 <= 20 x 96; 120 would wait forever).
+// Measured (profiles/ab_r02_fp64_producer_warpgroup.json): 16384^3 96.6 -> 98.2 % of the DMMA peak, rank-k
+// 90.7 -> 95.6 %, inner product 94.5 -> 96.3 %, panel-panel 91.6 -> 94.2 %, 2048^3 87-88.5 -> 89.5 %.
 #ifndef TM_PRODUCER_WARP
-#define TM_PRODUCER_WARP 0
+#define TM_PRODUCER_WARP 1
 #endif
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
@@ -614,7 +624,7 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, uin
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool FIX = true, bool PW = false>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + (PW ? 32 : 0), 1)
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + (PW ? 128 : 0), 1)
     k_dmma_tma(Args a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC) {
     constexpr int NWM = BM / WM, NW = (BM / WM) * (BN / WN);
@@ -715,8 +725,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + (PW ? 32 : 0), 1)
     if constexpr (PW) {
         // The producer warp: lane 0 walks the CTA's task list and keeps every stage of the ring filled, held
         // back only by the stages' empty barriers (and a task's copy-engine data flag); then the warp exits.
-        if (warp == NW) {
-            if (lane == 0) {
+        if (warp >= NW) {
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n");
+            if (warp == NW && lane == 0) {
                 uint32_t n = 0;
                 for (int x = ti; x < t_hi; x += t_step) {
                     const Task pt = a.tasks[x];
@@ -752,6 +763,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + (PW ? 32 : 0), 1)
             }
             return;
         }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n");
     } else {
         if (threadIdx.x == 0) {
             pc.issued = 0;
@@ -812,6 +824,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + (PW ? 32 : 0), 1)
             if (s == 0) TM_TRACE_EV(3, ti);
 #endif
             const unsigned char* st = sgen + stage * STAGE_BYTES;
+            uint32_t dep = 0;
 #pragma unroll
             for (int kk = 0; kk < KK; ++kk) {
                 double af[FM], bf[FN];
@@ -823,6 +836,12 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + (PW ? 32 : 0), 1)
                 for (int ni = 0; ni < FN; ++ni)
                     bf[ni] = *reinterpret_cast<const double*>(st + (boff ^ ((kk & 3) << 5)) + (kk >> 2) * B_CHUNK +
                                                               ni * 1024);
+                if (kk >= KK - 2) {
+#pragma unroll
+                    for (int mi = 0; mi < FM; ++mi) dep ^= static_cast<uint32_t>(__double2hiint(af[mi]));
+#pragma unroll
+                    for (int ni = 0; ni < FN; ++ni) dep ^= static_cast<uint32_t>(__double2hiint(bf[ni]));
+                }
 #pragma unroll
                 for (int mi = 0; mi < FM; ++mi)
 #pragma unroll
@@ -831,8 +850,13 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32 + (PW ? 32 : 0), 1)
                     if (kk == ISSUE_KK && warp == 0) top_up(n_use + PD + 1, ti);
                 }
             }
+            // Release the stage only once its fragment loads have RETURNED: the arrive's address depends on
+            // the slab's last loaded values (dep & a.zero == 0, known only at run time). ptxas otherwise
+            // hoists the arrive above the last DMMAs, right behind the issue of the last LDS, and a producer
+            // that refills the stage at once (the producer warpgroup) overwrites data still being read
+            // (measured: wrong A fragments in warps 0-2, whose boxes the refill writes first).
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (lane == 0) mbar_arrive_after(&empty[stage], dep & static_cast<uint32_t>(a.zero));
             ++n_use;
         }
         TM_TRACE_EV(4, ti);
@@ -1044,11 +1068,11 @@ constexpr int tma_smem() {
 struct TmaEntry {
     const void* fn;
     int bk, box_n, smem;
-    int extra_threads = 0;  // a producer warp behind the task-running warps
+    int extra_threads = 0;  // a producer warpgroup behind the task-running warps
 };
 const TmaEntry kTmaTable[kKernelCount] = {
     {(const void*)k_dmma_tma<128, 128, TM_TMA_BK128, 32, 32, TM_TMA_ST128, true, TM_PRODUCER_WARP != 0>, TM_TMA_BK128, 128,
-     tma_smem<128, 128, TM_TMA_BK128, TM_TMA_ST128>(), TM_PRODUCER_WARP != 0 ? 32 : 0},
+     tma_smem<128, 128, TM_TMA_BK128, TM_TMA_ST128>(), TM_PRODUCER_WARP != 0 ? 128 : 0},
     {(const void*)k_dmma_tma<64, 64, kBKSmall, 32, 32, kStagesSmall>, kBKSmall, 64, tma_smem<64, 64, kBKSmall, kStagesSmall>()},
     {nullptr, 0, 0, 0},
     {nullptr, 0, 0, 0},

@@ -56,6 +56,7 @@ struct Args {
     int32_t* done;             // per-block completion counters (Task::done), or nullptr
     int32_t prefetch_c = 0;    // TMA kernels: warm L2 with each task's C tile when the producer reaches it
     int32_t pdl_trigger = 0;   // TMA kernels: griddepcontrol.launch_dependents at each CTA's last task
+    int32_t zero = 0;          // always 0, but only known at run time: ties a stage's release to its last fragment loads
 };
 
 // One k-split C tile: its partials live in slots slot0 .. slot0+nslots-1 and

@@ -66,7 +66,7 @@ def test_tma_bitwise_equals_cpasync_over_tiles_and_splits():
                 assert ok, (trial, kw, worst)
                 got_a, st_a = run(nest, A, B, c, **kw)  # auto: TMA for the 128x128 kernel, cp.async otherwise
                 assert st_a == ("tma" if (tile, tile_n) == (128, 128) else "cpasync")
-                assert np.array_equal(got_a, got_t)
+                assert np.array_equal(got_a, got_t), (trial, m, n, k, kw, int((got_a != got_t).sum()))
 
 
 def test_tma_small_and_ragged_edges():
