@@ -284,3 +284,30 @@ def test_segments_and_programmatic_launch_are_bitwise_invisible():
     assert out["segments, PDL"][:2] == (2, "tma") and out["segments, stream order"][:2] == (2, "tma"), out
     assert out["cp.async, one launch"][:2] == (1, "cpasync"), out
     assert len({d for _, _, d in out.values()}) == 1, out
+
+
+def test_repeated_tma_launches_are_deterministic():
+    """Regression for the stage-release race the producer warpgroup exposed: the mbarrier
+    arrive that releases a stage was hoisted above the slab's last DMMAs, right behind the issue of its last
+    fragment loads, so a refill issued at once overwrote bytes still being read -- 30-60 % of 2048^3 launches
+    then differed from the cp.async kernel in whole A fragments of warps 0-2. Every launch must be bitwise
+    the cp.async result, launch after launch, for the unsplit, stream-K and uniformly split lowerings."""
+    for (m, n, k) in ((2048, 2048, 2048), (4096, 4096, 512)):
+        nest = fused_nest(m, n, k)
+        A = torch.empty(m * k, dtype=torch.float64, device="cuda")
+        B = torch.empty(k * n, dtype=torch.float64, device="cuda")
+        C0 = torch.empty(m * n, dtype=torch.float64, device="cuda")
+        T.fill_uniform_device(A, 11)
+        T.fill_uniform_device(B, 12)
+        T.fill_uniform_device(C0, 13)
+        for split in (1, 0, 3):
+            kw = dict(split_k=split, tile=128, tile_n=128)
+            ref = C0.clone()
+            T.execute(nest, A, B, ref, T.ExecOptions(staging="cpasync", **kw))
+            bad = 0
+            for _ in range(25):
+                Cd = C0.clone()
+                T.execute(nest, A, B, Cd, T.ExecOptions(staging="tma", **kw))
+                bad += int(not torch.equal(Cd, ref))
+            assert nest.last_launch()["staging"] == "tma"
+            assert bad == 0, (m, n, k, split, bad)
