@@ -1,4 +1,4 @@
-"""Stress: many repeated launches of the 128x128 TMA kernel, each compared bitwise with the cp.async result
+"""Stress: many repeated launches of the 128x128 TMA kernel, each compared bitwise with the cp.async result."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
