@@ -19,10 +19,11 @@
 // Staging variants of the DMMA kernel:
 //   k_dmma      — every thread issues 16-byte cp.async chunks of the slabs
 //                 into padded [k][m] / [n][k] stages;
-//   k_dmma_tma  — one thread issues TMA tensor copies (cp.async.bulk.tensor)
-//                 of the slabs into 128B-swizzled stages and runs ahead
-//                 across task boundaries (the next task's first slabs land
-//                 under this task's epilogue).
+//   k_dmma_tma  — one thread (of a producer warpgroup in the 128x128 kernel)
+//                 issues TMA tensor copies (cp.async.bulk.tensor) of the
+//                 slabs into 128B-swizzled stages and runs ahead across task
+//                 boundaries (the next task's first slabs land under this
+//                 task's epilogue).
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -573,24 +574,28 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 1) k_dmma(Args a) 
 // columns of the column-major A) lands as BM/16 boxes of 16 x BK doubles
 // ([k][16 m] rows of 128 B), B's slab (BK x BN) as BK/16 boxes of 16 x BN
 // ([n][16 k] rows), both with the 128-byte swizzle, so no padding and no
-// per-thread address arithmetic. One thread (warp 0, lane 0) is the
-// producer: it keeps STAGES-1 slabs in flight ahead of the slab being
-// consumed, following the CTA's task list across task boundaries, so the
-// next task's first slabs arrive while this task's C tile is written back;
-// entering a task it also warms L2 with that task's C tile (one bulk tensor
-// prefetch), so the C load at the task's start hits L2.
+// per-thread address arithmetic. One thread is the producer. In the 128x128
+// kernel it is lane 0 of a warp of its own (the producer warpgroup, PW; see
+// TM_PRODUCER_WARP below): it keeps every stage filled, held back only by
+// the stages' empty barriers, following the CTA's task list across task
+// boundaries, so the next task's first slabs arrive while this task's C
+// tile is written back; entering a task it also warms L2 with that task's C
+// tile (one bulk tensor prefetch), so the C load at the task's start hits
+// L2; a task's copy-engine data flag (Task::ready) it polls itself.
+// In the 128x64 / 64x64 variants (PW = false) the producer is lane 0 of DMMA
+// warp 0: it keeps STAGES-1 slabs in flight ahead of the slab being consumed
+// and issues the refill of a stage at k step TM_TMA_ISSUE_KK of the slab
+// after it (measured: step 2 beats steps 1 and 5 by 0.3-2 points); it does
+// not run ahead into a task whose data flag it has not seen.
 // full[s] completes on the TMA byte count; empty[s] on one arrive per warp.
-// The producer does not run ahead into a task whose copy-engine data flag
-// (Task::ready) it has not seen: that wait stays at the task boundary.
-// The refill of a stage is issued at k step TM_TMA_ISSUE_KK of the slab after
-// it (measured: step 2 beats steps 1 and 5 by 0.3-2 points).
 #ifndef TM_TMA_ISSUE_KK
 #define TM_TMA_ISSUE_KK 2
 #endif
 // Experiment knobs (tools/build_variant.sh; the product build leaves them at their defaults): the k-slab depth
 // and stage count of the 128x128 TMA kernel, and a start-up stagger of its warp groups (warps w, w+4, w+8,
-// w+12 share an SM sub-partition; group w/4 starts (NW/4-1 - w/4) * TM_STAGGER cycles late, so the producer's
-// warp 0 trails and the groups reach the task boundaries' C exchange one after the other).
+// w+12 share an SM sub-partition; group w/4 starts (NW/4-1 - w/4) * TM_STAGGER cycles late, so the groups reach
+// the task boundaries' C exchange one after the other). All measured and rejected:
+// profiles/ab_r02_fp64_slab_depth_stagger.json.
 #ifndef TM_TMA_BK128
 #define TM_TMA_BK128 32
 #endif

@@ -68,6 +68,7 @@ struct ReduceTile {
 
 enum Kernel : int {
     kDmma128 = 0,   // 128x128 C tile, 16 warps of 32x32 (4 per SM sub-partition), mma.sync m8n8k4 f64
+                    // (its TMA variant adds a producer warpgroup: 640 threads)
     kDmma64 = 1,    // 64x64 C tile, 4 warps of 32x32
     kFma64 = 2,     // 64x64, DFMA chain per entry (bit-exact vs sequential fma)
     kExact64 = 3,   // 64x64, DMUL + DADD per step (bit-exact vs the reference)
