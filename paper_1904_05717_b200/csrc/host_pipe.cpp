@@ -114,9 +114,9 @@ void pipe_order(const Extents& e, HostPipe& P) {
         const double Mi = static_cast<double>(at(mc, ni)), Nj = static_cast<double>(at(nc, nj)),
                      Kq = static_cast<double>(at(kc, nq)), M = static_cast<double>(e.m);
         // GEMM work enabled per element copied. A C column block is copied whole (all M rows, contiguous):
-        // cutting C into row blocks too would enable work sooner per byte, but the short runs of its 2-D
-        // copies cost more than that gains (16384^3: 262.4 ms against 259.2 with 2048-row blocks, 280.2 with
-        // 1024-row blocks whose runs are 8 KB; profiles/ab_r02_pipe_rowblocks.json).
+        // cutting C into row blocks too would enable work sooner per byte, but measured worse (16384^3:
+        // 262.4 ms against 259.2 with 2048-row blocks, 280.2 with 1024-row blocks;
+        // profiles/ab_r02_pipe_rowblocks.json).
         const double ri = ni < NI ? Nj : -1.0;
         const double rj = nj < NJ ? Mi * Kq / (M + Kq) : -1.0;
         const double rq = nq < NQ ? Mi * Nj / (Mi + Nj) : -1.0;
