@@ -87,7 +87,11 @@ void pipe_order(const Extents& e, HostPipe& P) {
     }();
     P.kcut = even_cuts(e.k, static_cast<int>(std::max<i64>(1, std::min<i64>(4, e.k / 4096))), 32);
     P.ncut = even_cuts(e.n, static_cast<int>(std::max<i64>(1, std::min<i64>(64, e.n / 256))), 128);
-    P.mcut = even_cuts(e.m, static_cast<int>(std::max<i64>(1, std::min<i64>(row_knob, e.m / 2048))), 128);
+    static const i64 row_min = [] {  // (TILEMUL_PIPE_ROWMIN: A/B knob; 512 measured +-2 % on 2048^3..4096^3)
+        const char* env = std::getenv("TILEMUL_PIPE_ROWMIN");
+        return env ? std::max<i64>(128, std::atoll(env)) : i64{2048};
+    }();
+    P.mcut = even_cuts(e.m, static_cast<int>(std::max<i64>(1, std::min<i64>(row_knob, e.m / row_min))), 128);
     P.steps.clear();
     const auto& mc = P.mcut;
     const auto& nc = P.ncut;
@@ -293,7 +297,16 @@ void execute_host(tm_plan* plan, const double* A, const double* B, double* C, co
     cudaStream_t st = plan->host_stream;
     tm_exec_opts o{};
     if (opts) o = *opts;
-    const bool pipelined = o.schedule == TM_SCHEDULE_FUSED && o.split_k <= 1 && (e.k >= 4096 || e.n >= 4096);
+    // Pipelined when there is enough to overlap: a long k or a wide n, or (round 2) any problem of >= 4 column
+    // blocks whose operands take >= ~1 ms on the bus (2048^3: 2.95 -> 2.52 ms, 3072^3: 7.05 -> 5.24 ms, 1536^3:
+    // 1.61 -> 1.52 ms; 1024^3, 25 MB, is slower pipelined: 0.71 -> 0.77 ms; TILEMUL_PIPE_MIN_MB: A/B knob).
+    static const double min_mb = [] {
+        const char* env = std::getenv("TILEMUL_PIPE_MIN_MB");
+        return env ? std::atof(env) : 48.0;
+    }();
+    const double mbytes = static_cast<double>(na + nb + nc) * 8.0 / 1e6;
+    const bool pipelined = o.schedule == TM_SCHEDULE_FUSED && o.split_k <= 1 &&
+                           (e.k >= 4096 || e.n >= 4096 || (e.n >= 1024 && mbytes >= min_mb));
     if (!pipelined) {
         cuda_check(cudaMemcpyAsync(plan->dA, A, na * sizeof(double), cudaMemcpyHostToDevice, st), "H2D A");
         cuda_check(cudaMemcpyAsync(plan->dB, B, nb * sizeof(double), cudaMemcpyHostToDevice, st), "H2D B");
