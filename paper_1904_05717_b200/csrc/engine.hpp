@@ -84,9 +84,11 @@ struct HostPipe {
         int q = 0;                           // ... of k-chunk q
     };
     std::vector<Step> steps;                 // in issue order
-    std::vector<int32_t> block_tasks;        // last-chunk tasks of each C column block
+    int done_rows = 1;                       // row blocks the downloads are cut into (1: whole column blocks)
+    std::vector<int32_t> block_tasks;        // last-chunk tasks of each C cell (column block b, row block i): [b * done_rows + i]
+    std::vector<std::pair<int, int>> cells;  // the C cells (b, i) in the order their last chunk is scheduled (download order)
     std::unique_ptr<Schedule> sched;
-    int32_t* flags = nullptr;  // [steps] data-ready flags, then [blocks] done counters
+    int32_t* flags = nullptr;  // [steps] data-ready flags, then [column blocks x row blocks] done counters
     int regions = 0;
     ~HostPipe() {
         if (flags) cudaFree(flags);

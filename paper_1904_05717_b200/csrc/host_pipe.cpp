@@ -85,7 +85,10 @@ void pipe_order(const Extents& e, HostPipe& P) {
         const char* env = std::getenv("TILEMUL_PIPE_ROWBLOCKS");
         return env ? std::max(1, std::atoi(env)) : 8;
     }();
-    P.kcut = even_cuts(e.k, static_cast<int>(std::max<i64>(1, std::min<i64>(4, e.k / 4096))), 32);
+    // (a small C, < 64 MB, costs nothing to revisit, and its few tiles make a chunk's tasks long: up to 32 chunks
+    // there, so the work left after the last upload is one short chunk -- 512^2 x 131072: 23.9 -> 20.x ms)
+    const i64 max_chunks = e.m * e.n * 8 < (i64{64} << 20) ? 32 : 4;
+    P.kcut = even_cuts(e.k, static_cast<int>(std::max<i64>(1, std::min<i64>(max_chunks, e.k / 4096))), 32);
     P.ncut = even_cuts(e.n, static_cast<int>(std::max<i64>(1, std::min<i64>(64, e.n / 256))), 128);
     static const i64 row_min = [] {  // (TILEMUL_PIPE_ROWMIN: A/B knob; 512 measured +-2 % on 2048^3..4096^3)
         const char* env = std::getenv("TILEMUL_PIPE_ROWMIN");
@@ -156,7 +159,9 @@ std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o,
     pipe_order(e, *P);
     const auto& nc = P->ncut;
     const auto& kc = P->kcut;
-    const int NJ = static_cast<int>(nc.size()) - 1, NQ = static_cast<int>(kc.size()) - 1;
+    const auto& mc = P->mcut;
+    const int NI = static_cast<int>(mc.size()) - 1, NJ = static_cast<int>(nc.size()) - 1,
+              NQ = static_cast<int>(kc.size()) - 1;
     tm_exec_opts uo = o;
     uo.split_k = 1;
     Nest first = plan.nest;
@@ -168,7 +173,12 @@ std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o,
     cuda_check(gpu::kernel_info(kernel, &info), "kernel_info");
     const i64 mt = cdiv(e.m, info.tile_m);
     P->regions = static_cast<int>(mt * cdiv(e.n, info.tile_n));
-    P->block_tasks.assign(static_cast<std::size_t>(NJ), 0);
+    // Downloads: whole column blocks (contiguous), unless C has too few of them to overlap anything -- a tall C
+    // (65536 x 256) goes back row block by row block. (Cutting every column block into row cells costs the
+    // C-dominated shapes: rank-k 16384^2 x 256 50.3 -> 57.1 ms, 16384^3 only 254.8 -> 254.4.)
+    P->done_rows = NJ < 8 ? NI : 1;
+    const int ND = P->done_rows;
+    P->block_tasks.assign(static_cast<std::size_t>(NJ) * static_cast<std::size_t>(ND), 0);
     auto sched = std::make_unique<Schedule>();
     sched->kernel = kernel;
     auto& T = sched->host_tasks;
@@ -186,11 +196,21 @@ std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o,
             tk.tile = static_cast<int32_t>(tk.i0 / info.tile_m + (tk.j0 / info.tile_n) * mt);
             tk.seq = sp.q;
             tk.ready = static_cast<int32_t>(u) + 1;
+            // its C cell: tiles never straddle a cut (cuts are multiples of 128, tiles 64 or 128 wide)
             const int b = static_cast<int>(std::upper_bound(nc.begin(), nc.end(), static_cast<i64>(tk.j0)) - nc.begin()) - 1;
-            tk.done = sp.q == NQ - 1 ? b + 1 : 0;
-            if (sp.q == NQ - 1) ++P->block_tasks[static_cast<std::size_t>(b)];
+            const int i = ND == 1 ? 0 : static_cast<int>(std::upper_bound(mc.begin(), mc.end(), static_cast<i64>(tk.i0)) - mc.begin()) - 1;
+            const int cell = b * ND + i;
+            tk.done = sp.q == NQ - 1 ? cell + 1 : 0;
+            if (sp.q == NQ - 1) ++P->block_tasks[static_cast<std::size_t>(cell)];
             T.push_back(tk);
         }
+        if (sp.q == NQ - 1)  // the cells this step finishes, in the order they go back to the host
+            for (int b = 0; b < NJ; ++b)
+                for (int i = 0; i < ND; ++i)
+                    if (nc[static_cast<std::size_t>(b)] >= sp.j0 && nc[static_cast<std::size_t>(b)] < sp.j1 &&
+                        (ND == 1 ? sp.i1 == e.m  // (a column block is done with the step that brings its last rows)
+                                 : mc[static_cast<std::size_t>(i)] >= sp.i0 && mc[static_cast<std::size_t>(i)] < sp.i1))
+                        P->cells.push_back({b, i});
     }
     if (T.size() > static_cast<std::size_t>(INT32_MAX)) fail_usage("too many tasks");
     sched->grid = std::max(1, std::min<int>(sm_count() * std::max(1, info.ctas_per_sm), static_cast<int>(T.size())));
@@ -200,7 +220,7 @@ std::unique_ptr<HostPipe> build_pipe(const tm_plan& plan, const tm_exec_opts& o,
     cuda_check(cudaMalloc(&sched->tasks, sizeof(gpu::Task) * T.size()), "cudaMalloc(tasks)");
     cuda_check(cudaMemcpyAsync(sched->tasks, T.data(), sizeof(gpu::Task) * T.size(), cudaMemcpyHostToDevice, st),
                "upload tasks");
-    cuda_check(cudaMalloc(&P->flags, sizeof(int32_t) * (P->steps.size() + static_cast<std::size_t>(NJ))),
+    cuda_check(cudaMalloc(&P->flags, sizeof(int32_t) * (P->steps.size() + P->block_tasks.size())),
                "cudaMalloc(pipeline flags)");
     cuda_check(cudaStreamSynchronize(st), "upload tasks (sync)");
     P->sched = std::move(sched);
@@ -222,7 +242,7 @@ void run_pipe(tm_plan* plan, const double* A, const double* B, double* C, const 
         plan->pipe = build_pipe(*plan, o, st);
     HostPipe& P = *plan->pipe;
     Schedule& S = *P.sched;
-    const std::size_t nu = P.steps.size(), nbk = P.ncut.size() - 1;
+    const std::size_t nu = P.steps.size(), nd = P.block_tasks.size(), ND = static_cast<std::size_t>(P.done_rows);
     if (plan->chunk_ready.empty()) {
         cudaEvent_t ev;
         cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
@@ -230,7 +250,7 @@ void run_pipe(tm_plan* plan, const double* A, const double* B, double* C, const 
     }
     cudaEvent_t zero = plan->chunk_ready[0];
     cuda_check(cudaMemsetAsync(S.progress, 0, sizeof(int32_t) * static_cast<std::size_t>(P.regions), st), "reset progress");
-    cuda_check(cudaMemsetAsync(P.flags, 0, sizeof(int32_t) * (nu + nbk), st), "reset flags");
+    cuda_check(cudaMemsetAsync(P.flags, 0, sizeof(int32_t) * (nu + nd), st), "reset flags");
     cuda_check(cudaEventRecord(zero, st), "event");
     const bool vec16 = e.m % 2 == 0 && e.k % 2 == 0 && origins_even(S.host_tasks);
     gpu::Args a{plan->dA, e.m, plan->dB, e.k, plan->dC, e.m, S.tasks, static_cast<int32_t>(S.host_tasks.size()),
@@ -258,16 +278,26 @@ void run_pipe(tm_plan* plan, const double* A, const double* B, double* C, const 
         cu_check(memops().write(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(P.flags + u), 1, 0),
                  "cuStreamWriteValue32");
     }
-    // each block goes back once its last unit's tasks are done
+    // each C cell (column block x row block) goes back once its last chunk's tasks are done, in the order
+    // the task list finishes them (a tall C -- 65536 x 256 -- goes back row block by row block under the uploads)
     cuda_check(cudaStreamWaitEvent(ds, zero, 0), "wait flags reset");
-    for (std::size_t b = 0; b < nbk; ++b) {
-        const i64 j0 = P.ncut[b], w = P.ncut[b + 1] - j0;
-        cu_check(memops().wait(reinterpret_cast<CUstream>(ds), reinterpret_cast<CUdeviceptr>(P.flags + nu + b),
-                               static_cast<cuuint32_t>(P.block_tasks[b]), CU_STREAM_WAIT_VALUE_GEQ),
+    for (const auto& [b, i] : P.cells) {
+        const std::size_t cell = static_cast<std::size_t>(b) * ND + static_cast<std::size_t>(i);
+        const i64 j0 = P.ncut[static_cast<std::size_t>(b)], w = P.ncut[static_cast<std::size_t>(b) + 1] - j0;
+        const i64 i0 = ND == 1 ? 0 : P.mcut[static_cast<std::size_t>(i)];
+        const i64 r = ND == 1 ? e.m : P.mcut[static_cast<std::size_t>(i) + 1] - i0;
+        cu_check(memops().wait(reinterpret_cast<CUstream>(ds), reinterpret_cast<CUdeviceptr>(P.flags + nu + cell),
+                               static_cast<cuuint32_t>(P.block_tasks[cell]), CU_STREAM_WAIT_VALUE_GEQ),
                  "cuStreamWaitValue32");
-        cuda_check(cudaMemcpyAsync(C + j0 * e.m, plan->dC + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
-                                   cudaMemcpyDeviceToHost, ds),
-                   "D2H C block");
+        if (r == e.m)
+            cuda_check(cudaMemcpyAsync(C + j0 * e.m, plan->dC + j0 * e.m, static_cast<std::size_t>(w * e.m) * 8,
+                                       cudaMemcpyDeviceToHost, ds),
+                       "D2H C block");
+        else
+            cuda_check(cudaMemcpy2DAsync(C + i0 + j0 * e.m, static_cast<std::size_t>(e.m) * 8, plan->dC + i0 + j0 * e.m,
+                                         static_cast<std::size_t>(e.m) * 8, static_cast<std::size_t>(r) * 8,
+                                         static_cast<std::size_t>(w), cudaMemcpyDeviceToHost, ds),
+                       "D2H C cell (2-D)");
     }
     cuda_check(cudaStreamSynchronize(ds), "execute_host sync");
     cuda_check(cudaStreamSynchronize(st), "execute_host sync");
@@ -298,7 +328,7 @@ void execute_host(tm_plan* plan, const double* A, const double* B, double* C, co
     tm_exec_opts o{};
     if (opts) o = *opts;
     // Pipelined when there is enough to overlap: a long k or a wide n, or (round 2) any problem of >= 4 column
-    // blocks whose operands take >= ~1 ms on the bus (2048^3: 2.95 -> 2.52 ms, 3072^3: 7.05 -> 5.24 ms, 1536^3:
+    // blocks or >= 4 row blocks whose operands take >= ~1 ms on the bus (2048^3: 2.95 -> 2.52 ms, 3072^3: 7.05 -> 5.24 ms, 1536^3:
     // 1.61 -> 1.52 ms; 1024^3, 25 MB, is slower pipelined: 0.71 -> 0.77 ms; TILEMUL_PIPE_MIN_MB: A/B knob).
     static const double min_mb = [] {
         const char* env = std::getenv("TILEMUL_PIPE_MIN_MB");
@@ -306,7 +336,7 @@ void execute_host(tm_plan* plan, const double* A, const double* B, double* C, co
     }();
     const double mbytes = static_cast<double>(na + nb + nc) * 8.0 / 1e6;
     const bool pipelined = o.schedule == TM_SCHEDULE_FUSED && o.split_k <= 1 &&
-                           (e.k >= 4096 || e.n >= 4096 || (e.n >= 1024 && mbytes >= min_mb));
+                           (e.k >= 4096 || e.n >= 4096 || ((e.n >= 1024 || e.m >= 8192) && mbytes >= min_mb));
     if (!pipelined) {
         cuda_check(cudaMemcpyAsync(plan->dA, A, na * sizeof(double), cudaMemcpyHostToDevice, st), "H2D A");
         cuda_check(cudaMemcpyAsync(plan->dB, B, nb * sizeof(double), cudaMemcpyHostToDevice, st), "H2D B");

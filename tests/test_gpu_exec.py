@@ -220,12 +220,14 @@ def test_large_shapes_sampled_entries(shape, name, split):
 @pytest.mark.parametrize("numerics,shape", [("dmma", (520, 2200, 8224)), ("exact", (520, 2200, 8224)),
                                             ("dmma", (4200, 640, 8224)), ("exact", (4200, 640, 8224)),
                                             ("dmma", (6200, 1100, 12320)),
-                                            ("dmma", (2048, 1280, 1100)), ("exact", (2048, 1280, 1100))])
+                                            ("dmma", (2048, 1280, 1100)), ("exact", (2048, 1280, 1100)),
+                                            ("dmma", (16400, 200, 520)), ("exact", (16400, 200, 520))])
 def test_host_buffer_pipeline_matches_device_path(numerics, shape):
     # 520 x 2200 x 8224: 2 k-chunks of 4128 / 4096, 8 column blocks of 384 (tail 296), one row block;
     # 4200 x 640 x 8224: 2 row blocks of A (2176 / 2024) x 2 column blocks x 2 k-chunks;
     # 6200 x 1100 x 12320: 3 row blocks x 4 column blocks x 3 k-chunks (every extension kind of the growing box);
-    # 2048 x 1280 x 1100: a small problem (50 MB of operands, one k-chunk, 5 column blocks), pipelined since round 2
+    # 2048 x 1280 x 1100: a small problem (50 MB of operands, one k-chunk, 5 column blocks), pipelined since round 2;
+    # 16400 x 200 x 520: a tall C (8 row blocks, one column block): uploaded and downloaded row block by row block
     m, n, k = shape
     hier = T.gpu_hierarchy(128)
     d = T.parse_name("C2A1C0")
